@@ -1,0 +1,298 @@
+"""Thin Python binding of the C-ABI in include/adct.h (argument marshalling only).
+
+Every step of the method runs in libadct.so's CUDA kernels; this module converts torch
+tensors / numpy arrays into pointers, geometries and status checks.  It never computes
+any part of the transform itself and there is no CPU fallback: if the library is missing
+the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libadct.so")
+
+U8, I16, I32, F32 = 0, 1, 2, 3
+CLIP_NONE, CLIP, CLIP_ROUND = 0, 1, 2
+
+_STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported matrix", 3: "singular", 4: "overflow",
+           5: "alignment", 6: "CUDA error", 7: "workspace"}
+
+SYMBOLS = [
+    "adct_matrix_create_int", "adct_matrix_create_real", "adct_matrix_info", "adct_matrix_destroy",
+    "adct_zigzag_order", "approx_dct8x8_fwd", "zonal_retain", "approx_dct8x8_inv", "psnr_reduce",
+    "approx_dct8x8_fused_sse", "adct_host_workspace_bytes", "approx_dct8x8_fused_sse_host",
+    "approx_dct8x8_fwd_quant", "adct_workspace_bytes", "adct_status_str", "adct_launch_count",
+]
+
+
+class AdctError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {_STATUS.get(status, status)} ({status})")
+        self.status = status
+
+
+class Geom(ctypes.Structure):
+    _fields_ = [("n_images", ctypes.c_int64), ("height", ctypes.c_int32), ("width", ctypes.c_int32),
+                ("image_stride", ctypes.c_int64), ("row_stride", ctypes.c_int64)]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built (run ./build.sh or __graft_entry__.build()); "
+                          "there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I32_, I64_, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    S = ctypes.c_int
+    L.adct_matrix_create_int.argtypes = [P, ctypes.POINTER(P)]
+    L.adct_matrix_create_real.argtypes = [P, ctypes.POINTER(P)]
+    L.adct_matrix_info.argtypes = [P, P, P, P, P, P, P, P]
+    L.adct_matrix_destroy.argtypes = [P]
+    L.adct_matrix_destroy.restype = None
+    L.adct_zigzag_order.argtypes = [P]
+    L.approx_dct8x8_fwd.argtypes = [P, P, S, Geom, P, S, P]
+    L.zonal_retain.argtypes = [P, S, I64_, I32_, P]
+    L.approx_dct8x8_inv.argtypes = [P, P, S, Geom, P, S, S, P]
+    L.psnr_reduce.argtypes = [P, S, P, S, Geom, D, S, P, P, P, ctypes.c_size_t, P]
+    L.approx_dct8x8_fused_sse.argtypes = [P, P, S, Geom, P, I32_, S, P, P, ctypes.c_size_t, P]
+    L.adct_host_workspace_bytes.argtypes = [Geom, I32_, I64_, S]
+    L.adct_host_workspace_bytes.restype = ctypes.c_size_t
+    L.approx_dct8x8_fused_sse_host.argtypes = [P, P, S, Geom, P, I32_, S, P, I64_, P, ctypes.c_size_t, P]
+    L.approx_dct8x8_fwd_quant.argtypes = [P, P, Geom, I32_, P, P]
+    L.adct_workspace_bytes.argtypes = [Geom, I32_]
+    L.adct_workspace_bytes.restype = ctypes.c_size_t
+    L.adct_status_str.argtypes = [S]
+    L.adct_status_str.restype = ctypes.c_char_p
+    L.adct_launch_count.argtypes = []
+    L.adct_launch_count.restype = I64_
+    for name in SYMBOLS:
+        fn = getattr(L, name)
+        if name not in ("adct_matrix_destroy", "adct_host_workspace_bytes", "adct_workspace_bytes",
+                        "adct_status_str", "adct_launch_count"):
+            fn.restype = S
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int, what: str) -> None:
+    if status != 0:
+        raise AdctError(status, what)
+
+
+_TORCH_DT = {torch.uint8: U8, torch.int16: I16, torch.int32: I32, torch.float32: F32}
+_DT_TORCH = {v: k for k, v in _TORCH_DT.items()}
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _TORCH_DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}") from None
+
+
+def geom_of(img: torch.Tensor) -> Geom:
+    """Geometry of an image stack [n, H, W] (or [H, W]) from its strides (elements)."""
+    if img.dim() == 2:
+        img = img.unsqueeze(0)
+    if img.dim() != 3 or img.stride(2) != 1:
+        raise ValueError("images must be [n, H, W] with unit column stride")
+    n, h, w = img.shape
+    return Geom(n, h, w, img.stride(0) if n > 1 else h * img.stride(1), img.stride(1))
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+@dataclass
+class MatrixInfo:
+    s: list
+    g: list
+    row_orthogonal: bool
+    is_integer: bool
+    max_abs_y_u8: int
+    max_abs_y_i16: int
+    specialized: bool
+
+
+class Matrix:
+    """A matrix descriptor (adct_matrix_create_int / adct_matrix_create_real)."""
+
+    def __init__(self, handle: int, name: str = ""):
+        self._h = ctypes.c_void_p(handle)
+        self.name = name
+
+    @classmethod
+    def from_int(cls, t, name: str = "") -> "Matrix":
+        arr = (ctypes.c_int32 * 64)(*[int(v) for v in list(t)])
+        h = ctypes.c_void_p()
+        _check(lib.adct_matrix_create_int(ctypes.cast(arr, ctypes.c_void_p), ctypes.byref(h)), "adct_matrix_create_int")
+        return cls(h.value, name)
+
+    @classmethod
+    def from_real(cls, c, name: str = "") -> "Matrix":
+        arr = (ctypes.c_double * 64)(*[float(v) for v in list(c)])
+        h = ctypes.c_void_p()
+        _check(lib.adct_matrix_create_real(ctypes.cast(arr, ctypes.c_void_p), ctypes.byref(h)), "adct_matrix_create_real")
+        return cls(h.value, name)
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if not self._h:
+            raise ValueError("matrix destroyed")
+        return self._h
+
+    def info(self) -> MatrixInfo:
+        s = (ctypes.c_double * 8)()
+        g = (ctypes.c_double * 64)()
+        ro, ii, sp = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        mu, mi = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.adct_matrix_info(self.handle, ctypes.cast(s, ctypes.c_void_p), ctypes.cast(g, ctypes.c_void_p),
+                                    ctypes.byref(ro), ctypes.byref(ii), ctypes.byref(mu), ctypes.byref(mi),
+                                    ctypes.byref(sp)), "adct_matrix_info")
+        return MatrixInfo(list(s), list(g), bool(ro.value), bool(ii.value), mu.value, mi.value, bool(sp.value))
+
+    def close(self) -> None:
+        if self._h:
+            lib.adct_matrix_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def zigzag_order() -> list:
+    o = (ctypes.c_int32 * 64)()
+    _check(lib.adct_zigzag_order(ctypes.cast(o, ctypes.c_void_p)), "adct_zigzag_order")
+    return list(o)
+
+
+def workspace_bytes(geom: Geom, n_r: int) -> int:
+    return int(lib.adct_workspace_bytes(geom, n_r))
+
+
+def launch_count() -> int:
+    return int(lib.adct_launch_count())
+
+
+# ---- the four calls -------------------------------------------------------------------------
+
+def approx_dct8x8_fwd(m: Matrix, src: torch.Tensor, coef_dtype=torch.int32, coef: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """Block-major coefficients [n, H/8, W/8, 8, 8] of every 8x8 block of src [n, H, W]."""
+    g = geom_of(src)
+    if coef is None:
+        coef = torch.empty((g.n_images, g.height // 8, g.width // 8, 8, 8), dtype=coef_dtype, device=src.device)
+    _check(lib.approx_dct8x8_fwd(m.handle, src.data_ptr(), dtype_code(src), g, coef.data_ptr(), dtype_code(coef),
+                                 _stream_ptr(stream)), "approx_dct8x8_fwd")
+    return coef
+
+
+def zonal_retain(coef: torch.Tensor, r: int, stream=None) -> torch.Tensor:
+    """Zero, in place, every coefficient at zig-zag position >= r."""
+    if not coef.is_contiguous():
+        raise ValueError("coefficients must be contiguous block-major")
+    _check(lib.zonal_retain(coef.data_ptr(), dtype_code(coef), coef.numel() // 64, int(r), _stream_ptr(stream)),
+           "zonal_retain")
+    return coef
+
+
+def approx_dct8x8_inv(m: Matrix, coef: torch.Tensor, height: int, width: int, recon_dtype=torch.float32,
+                      clip: int = CLIP_NONE, recon: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    n = coef.numel() // (height * width)
+    if recon is None:
+        recon = torch.empty((n, height, width), dtype=recon_dtype, device=coef.device)
+    g = geom_of(recon)
+    _check(lib.approx_dct8x8_inv(m.handle, coef.data_ptr(), dtype_code(coef), g, recon.data_ptr(),
+                                 dtype_code(recon), int(clip), _stream_ptr(stream)), "approx_dct8x8_inv")
+    return recon
+
+
+def psnr_reduce(orig: torch.Tensor, recon: torch.Tensor, peak: float = 255.0, clip: int = CLIP_NONE,
+                workspace: torch.Tensor | None = None, stream=None):
+    """(sse, psnr) fp64 per image."""
+    g = geom_of(orig)
+    gr = geom_of(recon)
+    if (gr.n_images, gr.height, gr.width, gr.row_stride) != (g.n_images, g.height, g.width, g.row_stride):
+        raise ValueError("orig and recon must share the geometry (strides in elements)")
+    sse = torch.empty(g.n_images, dtype=torch.float64, device=orig.device)
+    psnr = torch.empty(g.n_images, dtype=torch.float64, device=orig.device)
+    nbytes = workspace_bytes(g, 1)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=orig.device)
+    _check(lib.psnr_reduce(orig.data_ptr(), dtype_code(orig), recon.data_ptr(), dtype_code(recon), g, float(peak),
+                           int(clip), sse.data_ptr(), psnr.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                           _stream_ptr(stream)), "psnr_reduce")
+    return sse, psnr
+
+
+# ---- fused paths ------------------------------------------------------------------------------
+
+def approx_dct8x8_fused_sse(m: Matrix, src: torch.Tensor, r_list, clip: int = CLIP_NONE,
+                            workspace: torch.Tensor | None = None, sse: torch.Tensor | None = None,
+                            stream=None) -> torch.Tensor:
+    """SSE [n, len(r_list)] (fp64, device) of forward -> retain r -> inverse per image."""
+    g = geom_of(src)
+    rl = [int(r) for r in r_list]
+    arr = (ctypes.c_int32 * len(rl))(*rl)
+    if sse is None:
+        sse = torch.empty((g.n_images, len(rl)), dtype=torch.float64, device=src.device)
+    nbytes = workspace_bytes(g, len(rl))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=src.device)
+    _check(lib.approx_dct8x8_fused_sse(m.handle, src.data_ptr(), dtype_code(src), g,
+                                       ctypes.cast(arr, ctypes.c_void_p), len(rl), int(clip), sse.data_ptr(),
+                                       workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)),
+           "approx_dct8x8_fused_sse")
+    return sse
+
+
+def host_workspace_bytes(geom: Geom, n_r: int, chunk_images: int, src_dtype: int = U8) -> int:
+    return int(lib.adct_host_workspace_bytes(geom, n_r, chunk_images, src_dtype))
+
+
+def approx_dct8x8_fused_sse_host(m: Matrix, src_host: torch.Tensor, r_list, workspace: torch.Tensor,
+                                 chunk_images: int, clip: int = CLIP_NONE, sse_host: torch.Tensor | None = None,
+                                 stream=None) -> torch.Tensor:
+    """The fused path on a HOST image stack (pinned); returns host SSE [n, n_r]."""
+    g = geom_of(src_host)
+    rl = [int(r) for r in r_list]
+    arr = (ctypes.c_int32 * len(rl))(*rl)
+    if sse_host is None:
+        sse_host = torch.empty((g.n_images, len(rl)), dtype=torch.float64)
+    _check(lib.approx_dct8x8_fused_sse_host(m.handle, src_host.data_ptr(), dtype_code(src_host), g,
+                                            ctypes.cast(arr, ctypes.c_void_p), len(rl), int(clip),
+                                            sse_host.data_ptr(), int(chunk_images), workspace.data_ptr(),
+                                            workspace.numel(), _stream_ptr(stream)), "approx_dct8x8_fused_sse_host")
+    return sse_host
+
+
+def approx_dct8x8_fwd_quant(m: Matrix, src: torch.Tensor, step: int = 16, q: torch.Tensor | None = None,
+                            stream=None) -> torch.Tensor:
+    g = geom_of(src)
+    if q is None:
+        q = torch.empty((g.n_images, g.height // 8, g.width // 8, 8, 8), dtype=torch.int16, device=src.device)
+    _check(lib.approx_dct8x8_fwd_quant(m.handle, src.data_ptr(), g, int(step), q.data_ptr(), _stream_ptr(stream)),
+           "approx_dct8x8_fwd_quant")
+    return q
+
+
+def psnr_from_sse(sse: torch.Tensor, n_pixels: int, peak: float = 255.0) -> torch.Tensor:
+    """10 log10(peak^2 / (sse / n_pixels)); +inf where sse == 0 (host-side report helper)."""
+    mse = sse / float(n_pixels)
+    return torch.where(sse == 0, torch.full_like(sse, float("inf")), 10.0 * torch.log10(peak * peak / mse))

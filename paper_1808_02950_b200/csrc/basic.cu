@@ -1,0 +1,389 @@
+// basic.cu — the four calls of the method as separate kernels (§6.1):
+//   approx_dct8x8_fwd   B = C_hat A C_hat^T
+//   zonal_retain        first r in zig-zag order
+//   approx_dct8x8_inv   A = C_hat^T B' C_hat          P:L2237-2242 (C_hat^{-1}: reading A4)
+//   psnr_reduce         MSE / PSNR per image
+// plus the config-3 forward+quantiser.  One thread owns one 8x8 block; grid-stride loops
+// sized in multiples of the SM count.
+#include <cmath>
+
+#include "adct_host.h"
+
+namespace adct {
+namespace {
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+unsigned grid_for(int64_t work, int nt, int per_sm) {
+  const int64_t need = (work + nt - 1) / nt;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
+}
+
+template <typename SrcT>
+__device__ __forceinline__ void load_block(const SrcT* __restrict__ src, const KGeom& g, uint32_t b,
+                                           const FastDiv& dnbi, const FastDiv& dbw, float (&x)[8][8]) {
+  const uint32_t img = fdiv(b, dnbi);
+  const uint32_t q = b - img * g.nbi;
+  const uint32_t by = fdiv(q, dbw);
+  const uint32_t bx = q - by * g.bw;
+  const SrcT* p = src + (int64_t)img * g.image_stride + (int64_t)by * 8 * g.row_stride + (int64_t)bx * 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) Src<SrcT>::to_f(Src<SrcT>::load(p + (int64_t)i * g.row_stride), x[i]);
+}
+
+// ---- forward -----------------------------------------------------------------------------
+template <typename SrcT, typename OutT, class MP>
+__global__ void __launch_bounds__(256) fwd_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm,
+                                                  FastDiv dnbi, FastDiv dbw, uint32_t nblocks,
+                                                  OutT* __restrict__ coef) {
+  const MP m(dm);
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += gridDim.x * blockDim.x) {
+    float x[8][8], y[8][8];
+    load_block(src, g, b, dnbi, dbw, x);
+    fwd2d(m, x, y);
+    OutT* o = coef + (int64_t)b * 64;
+    if constexpr (sizeof(OutT) == 4 && !std::is_same<OutT, float>::value) {  // int32: exact Y
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int l = 0; l < 8; l += 4) {
+          int4 v = make_int4(__float2int_rn(y[k][l]), __float2int_rn(y[k][l + 1]), __float2int_rn(y[k][l + 2]),
+                             __float2int_rn(y[k][l + 3]));
+          *reinterpret_cast<int4*>(o + k * 8 + l) = v;
+        }
+    } else if constexpr (std::is_same<OutT, float>::value) {  // B = sb o Y
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int l = 0; l < 8; l += 4) {
+          float4 v = make_float4(y[k][l] * dm.sb[k * 8 + l], y[k][l + 1] * dm.sb[k * 8 + l + 1],
+                                 y[k][l + 2] * dm.sb[k * 8 + l + 2], y[k][l + 3] * dm.sb[k * 8 + l + 3]);
+          *reinterpret_cast<float4*>(o + k * 8 + l) = v;
+        }
+    } else {  // int16: exact Y (range checked on the host)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint4 v;
+        v.x = (uint32_t)(uint16_t)__float2int_rn(y[k][0]) | ((uint32_t)(uint16_t)__float2int_rn(y[k][1]) << 16);
+        v.y = (uint32_t)(uint16_t)__float2int_rn(y[k][2]) | ((uint32_t)(uint16_t)__float2int_rn(y[k][3]) << 16);
+        v.z = (uint32_t)(uint16_t)__float2int_rn(y[k][4]) | ((uint32_t)(uint16_t)__float2int_rn(y[k][5]) << 16);
+        v.w = (uint32_t)(uint16_t)__float2int_rn(y[k][6]) | ((uint32_t)(uint16_t)__float2int_rn(y[k][7]) << 16);
+        *reinterpret_cast<uint4*>(o + k * 8) = v;
+      }
+    }
+  }
+}
+
+// ---- zonal retention ------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) retain_kernel(T* __restrict__ coef, int64_t n_vec, uint64_t keep) {
+  constexpr int E = 16 / sizeof(T);  // elements per 16-byte vector
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n_vec; v += (int64_t)gridDim.x * blockDim.x) {
+    uint4 d = reinterpret_cast<uint4*>(coef)[v];
+    T* e = reinterpret_cast<T*>(&d);
+    const int pos0 = (int)((v * E) & 63);
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (!((keep >> (pos0 + i)) & 1ull)) e[i] = T(0);
+    reinterpret_cast<uint4*>(coef)[v] = d;
+  }
+}
+
+// ---- inverse ---------------------------------------------------------------------------------
+template <typename OutT>
+__device__ __forceinline__ void store_row(OutT* p, const float* x, int clip, float lo, float hi);
+
+template <>
+__device__ __forceinline__ void store_row<float>(float* p, const float* x, int clip, float lo, float hi) {
+  float v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    v[j] = x[j];
+    if (clip != ADCT_CLIP_NONE) v[j] = fminf(fmaxf(v[j], lo), hi);
+    if (clip == ADCT_CLIP_ROUND) v[j] = rintf(v[j]);
+  }
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+template <>
+__device__ __forceinline__ void store_row<uint8_t>(uint8_t* p, const float* x, int, float, float) {
+  uint32_t b[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) b[j] = (uint32_t)rintf(fminf(fmaxf(x[j], 0.0f), 255.0f));
+  uint2 v;
+  v.x = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+  v.y = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
+  *reinterpret_cast<uint2*>(p) = v;
+}
+template <>
+__device__ __forceinline__ void store_row<int16_t>(int16_t* p, const float* x, int, float, float) {
+  uint32_t b[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) b[j] = (uint32_t)(uint16_t)(int16_t)rintf(fminf(fmaxf(x[j], -32768.0f), 32767.0f));
+  uint4 v;
+  v.x = b[0] | (b[1] << 16);
+  v.y = b[2] | (b[3] << 16);
+  v.z = b[4] | (b[5] << 16);
+  v.w = b[6] | (b[7] << 16);
+  *reinterpret_cast<uint4*>(p) = v;
+}
+
+template <typename CoefT, typename OutT, class MP>
+__global__ void __launch_bounds__(256) inv_kernel(const CoefT* __restrict__ coef, KGeom g, DevMat dm,
+                                                  FastDiv dnbi, FastDiv dbw, uint32_t nblocks, int clip,
+                                                  float lo, float hi, OutT* __restrict__ recon) {
+  const MP m(dm);
+  constexpr bool kIntIn = !std::is_same<CoefT, float>::value;
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += gridDim.x * blockDim.x) {
+    float z[8][8], x[8][8];
+    const CoefT* c = coef + (int64_t)b * 64;
+    if constexpr (sizeof(CoefT) == 4) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int l = 0; l < 8; l += 4) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(c + k * 8 + l));
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float f = kIntIn ? (float)(int32_t)w[q] : __uint_as_float(w[q]);
+            z[k][l + q] = f * (kIntIn ? dm.wy[k * 8 + l + q] : dm.wb[k * 8 + l + q]);
+          }
+        }
+    } else {  // int16
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(c + k * 8));
+        float f[8];
+        i16row_to_f(v, f);
+#pragma unroll
+        for (int l = 0; l < 8; ++l) z[k][l] = f[l] * dm.wy[k * 8 + l];
+      }
+    }
+    inv2d<MP, ~0ull>(m, z, x);
+    const uint32_t img = fdiv(b, dnbi);
+    const uint32_t q = b - img * g.nbi;
+    const uint32_t by = fdiv(q, dbw);
+    const uint32_t bx = q - by * g.bw;
+    OutT* p = recon + (int64_t)img * g.image_stride + (int64_t)by * 8 * g.row_stride + (int64_t)bx * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) store_row<OutT>(p + (int64_t)i * g.row_stride, x[i], clip, lo, hi);
+  }
+}
+
+// ---- per-image squared error (deterministic two-level reduction) ------------------------------
+template <typename T>
+__device__ __forceinline__ float sample_at(const T* p) { return (float)*p; }
+
+template <typename OrigT, typename RecT>
+__global__ void __launch_bounds__(kRedNT) sse_kernel(const OrigT* __restrict__ orig, const RecT* __restrict__ rec,
+                                                     KGeom g, int32_t height, int32_t width, int clip, float lo,
+                                                     float hi, int32_t chunks, double* __restrict__ partial) {
+  __shared__ double red[kRedNT / 32];
+  const uint32_t img = blockIdx.y;
+  const int32_t r0 = blockIdx.x * kSseRows;
+  double acc = 0.0;
+  for (int32_t r = r0; r < r0 + kSseRows && r < height; ++r) {
+    const int64_t rowoff = (int64_t)img * g.image_stride + (int64_t)r * g.row_stride;
+    for (int32_t c = threadIdx.x; c < width; c += kRedNT) {
+      const float xo = (float)orig[rowoff + c];
+      float xr = (float)rec[rowoff + c];
+      if (clip != ADCT_CLIP_NONE) xr = fminf(fmaxf(xr, lo), hi);
+      if (clip == ADCT_CLIP_ROUND) xr = rintf(xr);
+      const double d = (double)xo - (double)xr;
+      acc = fma(d, d, acc);
+    }
+  }
+  const double tot = block_sum<kRedNT>(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)img * chunks + blockIdx.x] = tot;
+}
+
+__global__ void finalize_kernel(const double* __restrict__ partial, int32_t chunks, int64_t n_images,
+                                int32_t slots, SlotMap slot_of, int32_t n_out,
+                                double npix, double peak, double* __restrict__ sse, double* __restrict__ psnr) {
+  // one thread per (image, output): sums the image's chunk partials in chunk order
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_images * n_out) return;
+  const int64_t img = t / n_out;
+  const int32_t o = (int32_t)(t - img * n_out);
+  const int32_t s = slot_of.s[o];
+  double acc = 0.0;
+  if (s >= 0)
+    for (int32_t c = 0; c < chunks; ++c) acc += partial[((int64_t)img * chunks + c) * slots + s];
+  sse[t] = acc;
+  if (psnr) psnr[t] = acc == 0.0 ? INFINITY : 10.0 * log10(peak * peak / (acc / npix));
+}
+
+}  // namespace
+
+// exported to fused.cu
+void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
+                     int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st) {
+  const int64_t n = n_images * n_out;
+  if (n == 0) return;
+  finalize_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(partial, chunks, n_images, slots, slot_of, n_out,
+                                                                npix, peak, sse, psnr);
+  count_launch();
+}
+
+}  // namespace adct
+
+using namespace adct;
+
+namespace {
+
+template <typename SrcT, typename OutT>
+adct_status launch_fwd(const adct_matrix* m, const void* src, const adct_geom& g, void* coef, cudaStream_t st) {
+  const KGeom kg = make_kgeom(g);
+  const uint32_t nb = (uint32_t)(g.n_images * kg.nbi);
+  if (nb == 0) return ADCT_OK;
+  const FastDiv dnbi = make_fastdiv(kg.nbi), dbw = make_fastdiv(kg.bw);
+  const unsigned grid = grid_for(nb, 256, 8);
+  if (m->specialized)
+    fwd_kernel<SrcT, OutT, T1Mat><<<grid, 256, 0, st>>>((const SrcT*)src, kg, m->dev, dnbi, dbw, nb, (OutT*)coef);
+  else
+    fwd_kernel<SrcT, OutT, RtMat><<<grid, 256, 0, st>>>((const SrcT*)src, kg, m->dev, dnbi, dbw, nb, (OutT*)coef);
+  count_launch();
+  return launch_status();
+}
+
+template <typename CoefT, typename OutT>
+adct_status launch_inv(const adct_matrix* m, const void* coef, const adct_geom& g, void* recon, adct_clip clip,
+                       float lo, float hi, cudaStream_t st) {
+  const KGeom kg = make_kgeom(g);
+  const uint32_t nb = (uint32_t)(g.n_images * kg.nbi);
+  if (nb == 0) return ADCT_OK;
+  const FastDiv dnbi = make_fastdiv(kg.nbi), dbw = make_fastdiv(kg.bw);
+  const unsigned grid = grid_for(nb, 256, 8);
+  if (m->specialized)
+    inv_kernel<CoefT, OutT, T1Mat><<<grid, 256, 0, st>>>((const CoefT*)coef, kg, m->dev, dnbi, dbw, nb, (int)clip,
+                                                         lo, hi, (OutT*)recon);
+  else
+    inv_kernel<CoefT, OutT, RtMat><<<grid, 256, 0, st>>>((const CoefT*)coef, kg, m->dev, dnbi, dbw, nb, (int)clip,
+                                                         lo, hi, (OutT*)recon);
+  count_launch();
+  return launch_status();
+}
+
+template <typename OrigT, typename RecT>
+void launch_sse(const void* orig, const void* rec, const adct_geom& g, int clip, float lo, float hi, double* partial,
+                int32_t chunks, cudaStream_t st) {
+  dim3 grid((unsigned)chunks, (unsigned)g.n_images);
+  sse_kernel<OrigT, RecT><<<grid, kRedNT, 0, st>>>((const OrigT*)orig, (const RecT*)rec, make_kgeom(g), g.height,
+                                                   g.width, clip, lo, hi, chunks, partial);
+  count_launch();
+}
+
+}  // namespace
+
+extern "C" {
+
+adct_status approx_dct8x8_fwd(const adct_matrix* m, const void* src, adct_dtype src_t, adct_geom g, void* coef,
+                              adct_dtype coef_t, void* stream) {
+  if (!m || !src || !coef) return ADCT_E_INVALID_ARGUMENT;
+  if (adct_status s = check_geom(g)) return s;
+  if (src_t != ADCT_U8 && src_t != ADCT_I16) return ADCT_E_INVALID_ARGUMENT;
+  if (coef_t != ADCT_I32 && coef_t != ADCT_I16 && coef_t != ADCT_F32) return ADCT_E_INVALID_ARGUMENT;
+  if (!aligned(src, src_t == ADCT_U8 ? 8 : 16) || !aligned(coef, 16)) return ADCT_E_ALIGNMENT;
+  if (coef_t != ADCT_F32) {
+    if (!m->is_int) return ADCT_E_OVERFLOW;
+    const int64_t bound = src_t == ADCT_U8 ? m->max_u8 : m->max_i16;
+    if (coef_t == ADCT_I16 && bound > 32767) return ADCT_E_OVERFLOW;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (src_t == ADCT_U8) {
+    if (coef_t == ADCT_I32) return launch_fwd<uint8_t, int32_t>(m, src, g, coef, st);
+    if (coef_t == ADCT_I16) return launch_fwd<uint8_t, int16_t>(m, src, g, coef, st);
+    return launch_fwd<uint8_t, float>(m, src, g, coef, st);
+  }
+  if (coef_t == ADCT_I32) return launch_fwd<int16_t, int32_t>(m, src, g, coef, st);
+  if (coef_t == ADCT_I16) return launch_fwd<int16_t, int16_t>(m, src, g, coef, st);
+  return launch_fwd<int16_t, float>(m, src, g, coef, st);
+}
+
+adct_status zonal_retain(void* coef, adct_dtype coef_t, int64_t n_blocks, int32_t r, void* stream) {
+  if (!coef || n_blocks < 0) return ADCT_E_INVALID_ARGUMENT;
+  if (r < 1 || r > 64) return ADCT_E_INVALID_ARGUMENT;
+  if (coef_t != ADCT_I32 && coef_t != ADCT_I16 && coef_t != ADCT_F32) return ADCT_E_INVALID_ARGUMENT;
+  if (!aligned(coef, 16)) return ADCT_E_ALIGNMENT;
+  if (n_blocks == 0) return ADCT_OK;
+  const uint64_t keep = keep_mask(r);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int esz = coef_t == ADCT_I16 ? 2 : 4;
+  const int64_t n_vec = n_blocks * 64 * esz / 16;
+  const unsigned grid = grid_for(n_vec, 256, 16);
+  if (esz == 2)
+    retain_kernel<int16_t><<<grid, 256, 0, st>>>((int16_t*)coef, n_vec, keep);
+  else
+    retain_kernel<int32_t><<<grid, 256, 0, st>>>((int32_t*)coef, n_vec, keep);
+  count_launch();
+  return launch_status();
+}
+
+adct_status approx_dct8x8_inv(const adct_matrix* m, const void* coef, adct_dtype coef_t, adct_geom g, void* recon,
+                              adct_dtype recon_t, adct_clip clip, void* stream) {
+  if (!m || !coef || !recon) return ADCT_E_INVALID_ARGUMENT;
+  if (adct_status s = check_geom(g)) return s;
+  if (coef_t != ADCT_I32 && coef_t != ADCT_I16 && coef_t != ADCT_F32) return ADCT_E_INVALID_ARGUMENT;
+  if (coef_t != ADCT_F32 && !m->is_int) return ADCT_E_INVALID_ARGUMENT;
+  if (clip != ADCT_CLIP_NONE && clip != ADCT_CLIP && clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  if (recon_t == ADCT_U8 || recon_t == ADCT_I16) {
+    if (clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  } else if (recon_t != ADCT_F32) {
+    return ADCT_E_INVALID_ARGUMENT;
+  }
+  const int rb = recon_t == ADCT_U8 ? 8 : 16;
+  if (!aligned(coef, 16) || !aligned(recon, rb)) return ADCT_E_ALIGNMENT;
+  // F32 reconstructions clip to the range of 8-bit images (the paper's setting)
+  const float lo = recon_t == ADCT_I16 ? -32768.0f : 0.0f, hi = recon_t == ADCT_I16 ? 32767.0f : 255.0f;
+  cudaStream_t st = (cudaStream_t)stream;
+#define ADCT_INV_DISPATCH(CT)                                                                  \
+  if (recon_t == ADCT_F32) return launch_inv<CT, float>(m, coef, g, recon, clip, lo, hi, st);  \
+  if (recon_t == ADCT_U8) return launch_inv<CT, uint8_t>(m, coef, g, recon, clip, lo, hi, st); \
+  return launch_inv<CT, int16_t>(m, coef, g, recon, clip, lo, hi, st);
+  if (coef_t == ADCT_I32) { ADCT_INV_DISPATCH(int32_t) }
+  if (coef_t == ADCT_I16) { ADCT_INV_DISPATCH(int16_t) }
+  ADCT_INV_DISPATCH(float)
+#undef ADCT_INV_DISPATCH
+}
+
+adct_status psnr_reduce(const void* orig, adct_dtype orig_t, const void* recon, adct_dtype recon_t, adct_geom g,
+                        double peak, adct_clip clip, double* sse, double* psnr, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  if (!orig || !recon || !sse) return ADCT_E_INVALID_ARGUMENT;
+  if (adct_status s = check_geom(g)) return s;
+  if (orig_t != ADCT_U8 && orig_t != ADCT_I16) return ADCT_E_INVALID_ARGUMENT;
+  if (recon_t != ADCT_U8 && recon_t != ADCT_I16 && recon_t != ADCT_F32) return ADCT_E_INVALID_ARGUMENT;
+  if (!(peak > 0.0)) return ADCT_E_INVALID_ARGUMENT;
+  if (!workspace || workspace_bytes < adct_workspace_bytes(g, 1)) return ADCT_E_WORKSPACE;
+  if (g.n_images == 0) return ADCT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int32_t chunks = (int32_t)sse_chunks(g);
+  double* partial = (double*)workspace;
+  const float lo = orig_t == ADCT_U8 ? 0.0f : -32768.0f, hi = orig_t == ADCT_U8 ? 255.0f : 32767.0f;
+  const int c = (int)clip;
+  if (orig_t == ADCT_U8) {
+    if (recon_t == ADCT_F32) launch_sse<uint8_t, float>(orig, recon, g, c, lo, hi, partial, chunks, st);
+    else if (recon_t == ADCT_U8) launch_sse<uint8_t, uint8_t>(orig, recon, g, c, lo, hi, partial, chunks, st);
+    else launch_sse<uint8_t, int16_t>(orig, recon, g, c, lo, hi, partial, chunks, st);
+  } else {
+    if (recon_t == ADCT_F32) launch_sse<int16_t, float>(orig, recon, g, c, lo, hi, partial, chunks, st);
+    else if (recon_t == ADCT_U8) launch_sse<int16_t, uint8_t>(orig, recon, g, c, lo, hi, partial, chunks, st);
+    else launch_sse<int16_t, int16_t>(orig, recon, g, c, lo, hi, partial, chunks, st);
+  }
+  SlotMap sm{};
+  launch_finalize(partial, chunks, g.n_images, 1, sm, 1, (double)g.height * g.width, peak, sse, psnr, st);
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,598 @@
+// fused.cu — the performance paths: forward -> zonal retention -> inverse -> squared error
+// per image with every block read once (§6.1), the host-buffer
+// pipeline around it, and the config-3 forward + quantiser.
+//
+// Deterministic reductions: CTA (chunk c of image i) owns blocks [c*NT*BPT, (c+1)*NT*BPT)
+// of image i in raster order; each thread's fp64 sum is reduced in a fixed shuffle/smem
+// order into partial[i][c][slot]; a finalize kernel adds the chunks of an image in order.
+// Results therefore do not depend on scheduling, and sharding images over GPUs gives the
+// same per-image sums bit for bit.
+#include <cmath>
+#include <mutex>
+
+#include "adct_host.h"
+
+namespace adct {
+
+void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
+                     int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st);
+
+namespace {
+
+constexpr int NT = kRedNT;
+constexpr int BPT = kFusedBPT;
+constexpr int BPT_U8 = kFusedBPTU8;
+
+__host__ __device__ constexpr int popc64(uint64_t v) {
+  int c = 0;
+  for (int i = 0; i < 64; ++i) c += (int)((v >> i) & 1u);
+  return c;
+}
+
+template <int CLIP>
+__device__ __forceinline__ float clipv(float v, float lo, float hi) {
+  if (CLIP == ADCT_CLIP_NONE) return v;
+  v = fminf(fmaxf(v, lo), hi);
+  if (CLIP == ADCT_CLIP_ROUND) v = rintf(v);
+  return v;
+}
+
+template <typename SrcT>
+__device__ __forceinline__ void load_rows(const SrcT* __restrict__ base, const KGeom& g, const FastDiv& dbw,
+                                          uint32_t q, typename Src<SrcT>::Row (&r)[8]) {
+  const uint32_t by = fdiv(q, dbw);
+  const uint32_t bx = q - by * g.bw;
+  const SrcT* p = base + (int64_t)by * 8 * g.row_stride + (int64_t)bx * 8;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = Src<SrcT>::load(p + (int64_t)i * g.row_stride);
+}
+
+// ---- single r, compile-time retention pattern ------------------------------------------
+// r <= 32: reconstruct from the kept coefficients, e = x - x_hat.
+// r >  32: inverse of the dropped coefficients, e = H (W o Y o drop) H^T = x - x_hat
+//          (exactly 0 at r = 64, reading A17).
+template <typename SrcT, class MP, int R, int CLIP>
+__device__ __forceinline__ float block_sse(const MP& m, const typename Src<SrcT>::Row (&rows)[8]) {
+  constexpr uint64_t KEEP = keep_mask(R);
+  constexpr bool RESID = popc64(KEEP) > 32;
+  constexpr uint64_t NZ = RESID ? ~KEEP : KEEP;
+  float x[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) Src<SrcT>::to_f(rows[i], x[i]);
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  if constexpr (NZ == 0) {
+    return 0.0f;  // r = 64: nothing dropped, x_hat = x
+  } else {
+    float y[8][8];
+    fwd2d(m, x, y);
+    float z[8][8], xh[8][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int l = 0; l < 8; ++l) z[k][l] = ((NZ >> (k * 8 + l)) & 1ull) ? y[k][l] * m.wy(k, l) : 0.0f;
+    inv2d<MP, NZ>(m, z, xh);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float d;
+        if constexpr (RESID) d = (CLIP == ADCT_CLIP_NONE) ? xh[i][j] : x[i][j] - clipv<CLIP>(x[i][j] - xh[i][j], Src<SrcT>::lo, Src<SrcT>::hi);
+        else d = x[i][j] - clipv<CLIP>(xh[i][j], Src<SrcT>::lo, Src<SrcT>::hi);
+        acc[j & 3] = fmaf(d, d, acc[j & 3]);
+      }
+  }
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// ---- the hot path: u8 samples, integer matrix, no clip ----------------------------------------
+// Samples are turned into fp32 with one PRMT each (bit pattern 0x4700xx00 = M + x, M = 2^15;
+// every intermediate stays an integer below 2^24, so the forward is still exact).  The vertical
+// butterflies s_i = x_i + x_{7-i}, t_i = x_i - x_{7-i} of the forward are kept and reused by
+// the error: with the inverse's last butterfly x_hat_i = E_i + O_i, x_hat_{7-i} = E_i - O_i,
+//   (x_i - x_hat_i)^2 + (x_{7-i} - x_hat_{7-i})^2 = ((s_i - 2E_i)^2 + (t_i - 2O_i)^2) / 2,
+// so each pixel pair costs two differences and two squares.  The weights carry the factor 2.
+__host__ __device__ constexpr uint32_t row_mask(uint64_t nz) {
+  uint32_t r = 0;
+  for (int k = 0; k < 8; ++k)
+    if ((nz >> (8 * k)) & 0xffull) r |= 1u << k;
+  return r;
+}
+
+// the selector is an immediate and the magic 0x47000000 a register (set once per thread),
+// so each sample costs exactly one PRMT
+template <uint32_t SEL>
+__device__ __forceinline__ float px_f(uint32_t w, uint32_t magic) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(magic), "n"(SEL));
+  return __uint_as_float(r);
+}
+
+
+template <class MP, int R>
+__device__ __forceinline__ float block_sse_u8(const MP& m, const uint2 (&rows)[8], uint32_t magic) {
+  constexpr uint64_t KEEP = keep_mask(R);
+  constexpr bool RESID = popc64(KEEP) > 32;
+  constexpr uint64_t NZ = RESID ? ~KEEP : KEEP;
+  constexpr uint32_t ROWS = row_mask(NZ);
+  if constexpr (NZ == 0) {
+    return 0.0f;
+  } else {
+    float sv[4][8], tv[4][8], p[8][8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float xc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t w = j < 4 ? rows[i].x : rows[i].y;
+        switch (j & 3) {
+          case 0: xc[i] = px_f<0x7504u>(w, magic); break;
+          case 1: xc[i] = px_f<0x7514u>(w, magic); break;
+          case 2: xc[i] = px_f<0x7524u>(w, magic); break;
+          default: xc[i] = px_f<0x7534u>(w, magic); break;
+        }
+      }
+      float s[4], t[4], col[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        s[i] = xc[i] + xc[7 - i];
+        t[i] = xc[i] - xc[7 - i];
+        sv[i][j] = s[i] - 2.0f * kSampleBias;
+        tv[i][j] = t[i];
+      }
+      fwd8_st(m, s, t, col);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[k][j] = col[k];
+    }
+    float q[8][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (!((ROWS >> k) & 1u)) continue;
+      float y[8], z[8];
+      fwd8(m, p[k], y);
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? (y[l] - m.ybias(k, l)) * m.wy2(k, l) : 0.0f;
+#define ADCT_ROWINV(K)                                                          \
+  if (k == K) {                                                                 \
+    constexpr uint32_t rm = (uint32_t)((NZ >> (8 * K)) & 0xffull);              \
+    if constexpr (rm != 0) inv8<MP, rm>(m, z, q[K]);                            \
+  }
+      ADCT_ROWINV(0) ADCT_ROWINV(1) ADCT_ROWINV(2) ADCT_ROWINV(3)
+      ADCT_ROWINV(4) ADCT_ROWINV(5) ADCT_ROWINV(6) ADCT_ROWINV(7)
+#undef ADCT_ROWINV
+    }
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float col[8], e[4], o[4];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) col[k] = ((ROWS >> k) & 1u) ? q[k][j] : 0.0f;
+      inv8_eo<MP, ROWS>(m, col, e, o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if constexpr (RESID) {
+          acc[i] = fmaf(e[i], e[i], acc[i]);
+          acc[i] = fmaf(o[i], o[i], acc[i]);
+        } else {
+          const float dp = sv[i][j] - e[i], dm = tv[i][j] - o[i];
+          acc[i] = fmaf(dp, dp, acc[i]);
+          acc[i] = fmaf(dm, dm, acc[i]);
+        }
+      }
+    }
+    return 0.5f * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+  }
+}
+
+template <class MP, int R>
+__global__ void __launch_bounds__(NT) fused_u8_kernel(const uint8_t* __restrict__ src, KGeom g, DevMat dm,
+                                                      FastDiv dbw, int32_t chunks, double* __restrict__ partial,
+                                                      uint32_t magic /* 0x47000000, kept in a register */) {
+  __shared__ double red[NT / 32];
+  const MP m(dm);
+  const uint8_t* base = src + (int64_t)blockIdx.y * g.image_stride;
+  const uint32_t q0 = blockIdx.x * (NT * BPT_U8) + threadIdx.x;
+  uint2 a[8], b[8], c[8];
+  double acc = 0.0;
+  if (q0 < g.nbi) load_rows(base, g, dbw, q0, a);
+  if (q0 + NT < g.nbi) load_rows(base, g, dbw, q0 + NT, b);
+#pragma unroll 1
+  for (int mb = 0; mb < BPT_U8; mb += 3) {
+    const uint32_t qa = q0 + mb * NT, qb = qa + NT, qc = qb + NT;
+    if (qc < g.nbi) load_rows(base, g, dbw, qc, c);
+    if (qa < g.nbi) acc += (double)block_sse_u8<MP, R>(m, a, magic);
+    if (mb + 3 < BPT_U8 && qc + NT < g.nbi) load_rows(base, g, dbw, qc + NT, a);
+    if (qb < g.nbi) acc += (double)block_sse_u8<MP, R>(m, b, magic);
+    if (mb + 4 < BPT_U8 && qc + 2 * NT < g.nbi) load_rows(base, g, dbw, qc + 2 * NT, b);
+    if (qc < g.nbi) acc += (double)block_sse_u8<MP, R>(m, c, magic);
+  }
+  const double tot = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * chunks + blockIdx.x] = tot;
+}
+
+template <typename SrcT, class MP, int R, int CLIP>
+__global__ void __launch_bounds__(NT) fused_single_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm,
+                                                          FastDiv dbw, int32_t chunks,
+                                                          double* __restrict__ partial) {
+  __shared__ double red[NT / 32];
+  const MP m(dm);
+  const SrcT* base = src + (int64_t)blockIdx.y * g.image_stride;
+  const uint32_t q0 = blockIdx.x * (NT * BPT) + threadIdx.x;
+  using Row = typename Src<SrcT>::Row;
+  Row a[8], b[8];
+  double acc = 0.0;
+  if (q0 < g.nbi) load_rows(base, g, dbw, q0, a);
+#pragma unroll 1
+  for (int mb = 0; mb < BPT; mb += 2) {
+    const uint32_t qa = q0 + mb * NT, qb = qa + NT, qc = qb + NT;
+    if (qb < g.nbi) load_rows(base, g, dbw, qb, b);
+    if (qa < g.nbi) acc += (double)block_sse<SrcT, MP, R, CLIP>(m, a);
+    if (mb + 2 < BPT && qc < g.nbi) load_rows(base, g, dbw, qc, a);
+    if (qb < g.nbi) acc += (double)block_sse<SrcT, MP, R, CLIP>(m, b);
+  }
+  const double tot = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * chunks + blockIdx.x] = tot;
+}
+
+// ---- any list of r: incremental inverse of the dropped coefficients ----------------------
+// Coefficients are added in decreasing zig-zag rank z = 63..1; after adding rank z the
+// register block e = H (W o Y o [rank >= z]) H^T is x - x_hat for r = z.  Each step is a
+// rank-one update e += (w y)_z h_k h_l^T (the inverse applied to one coefficient).
+template <typename SrcT, class MP, int CLIP>
+__global__ void __launch_bounds__(NT) fused_sweep_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm,
+                                                         FastDiv dbw, int32_t chunks, uint64_t rmask, int32_t rmin,
+                                                         double* __restrict__ partial) {
+  __shared__ float zacc[64][NT];
+  __shared__ double red[NT / 32];
+  const MP m(dm);
+#pragma unroll
+  for (int z = 0; z < 64; ++z) zacc[z][threadIdx.x] = 0.0f;
+  const SrcT* base = src + (int64_t)blockIdx.y * g.image_stride;
+  const uint32_t q0 = blockIdx.x * (NT * BPT) + threadIdx.x;
+#pragma unroll 1
+  for (int mb = 0; mb < BPT; ++mb) {
+    const uint32_t q = q0 + mb * NT;
+    if (q >= g.nbi) break;
+    typename Src<SrcT>::Row rows[8];
+    load_rows(base, g, dbw, q, rows);
+    float x[8][8], y[8][8], e[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) Src<SrcT>::to_f(rows[i], x[i]);
+    fwd2d(m, x, y);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) e[i][j] = 0.0f;
+#pragma unroll
+    for (int zr = 63; zr >= 1; --zr) {
+      if (zr < rmin) break;
+      const int pos = zz_order_at(zr);
+      const int k = pos >> 3, l = pos & 7;
+      const float c = y[k][l] * m.wy(k, l);
+      float a[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fmac<MP>(m.h(i, k), c, -0.0f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[i][j] = fmac<MP>(m.h(j, l), a[i], e[i][j]);
+      if ((rmask >> zr) & 1ull) {
+        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float d = (CLIP == ADCT_CLIP_NONE)
+                                ? e[i][j]
+                                : x[i][j] - clipv<CLIP>(x[i][j] - e[i][j], Src<SrcT>::lo, Src<SrcT>::hi);
+            s[j & 3] = fmaf(d, d, s[j & 3]);
+          }
+        zacc[zr - 1][threadIdx.x] += (s[0] + s[1]) + (s[2] + s[3]);
+      }
+    }
+  }
+  __syncthreads();
+  // r = z+1 slots 0..62 (slot 63, r = 64, stays 0: nothing dropped)
+  for (int z = 0; z < 64; ++z) {
+    if (z == 63 || !((rmask >> (z + 1)) & 1ull)) {
+      if (threadIdx.x == 0) partial[((int64_t)blockIdx.y * chunks + blockIdx.x) * 64 + z] = 0.0;
+      continue;
+    }
+    const double tot = block_sum<NT>((double)zacc[z][threadIdx.x], red);
+    if (threadIdx.x == 0) partial[((int64_t)blockIdx.y * chunks + blockIdx.x) * 64 + z] = tot;
+  }
+}
+
+// ---- config 3: forward with S folded into a uniform quantiser ------------------------------
+// q = sign(Y) floor(|Y| / (step sqrt(n_k n_l)) + 1/2) (reading A10).  fp32 estimate; when the
+// estimate is within 1e-4 of a rounding boundary the exact integer rule
+// (2m-1)^2 step^2 n_k n_l <= 4 Y^2 < (2m+1)^2 step^2 n_k n_l decides (in fp64, exact below 2^53).
+template <class MP>
+__global__ void __launch_bounds__(256) fwd_quant_kernel(const uint8_t* __restrict__ src, KGeom g, DevMat dm,
+                                                        FastDiv dnbi, FastDiv dbw, uint32_t nblocks,
+                                                        int16_t* __restrict__ out) {
+  const MP m(dm);
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += gridDim.x * blockDim.x) {
+    const uint32_t img = fdiv(b, dnbi);
+    const uint32_t q = b - img * g.nbi;
+    const uint32_t by = fdiv(q, dbw);
+    const uint32_t bx = q - by * g.bw;
+    const uint8_t* p = src + (int64_t)img * g.image_stride + (int64_t)by * 8 * g.row_stride + (int64_t)bx * 8;
+    float x[8][8], y[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u8row_to_f(ldg_u8row(p + (int64_t)i * g.row_stride), x[i]);
+    fwd2d(m, x, y);
+    int16_t* o = out + (int64_t)b * 64;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t w[4];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) {
+        const float a = fabsf(y[k][l]);
+        const float t = fmaf(a, dm.q_inv[k * 8 + l], 0.5f);
+        float mq = floorf(t);
+        const float fr = t - mq;
+        if (fr < 1e-4f || fr > 1.0f - 1e-4f) {  // near a boundary: exact decision
+          const double a2 = 4.0 * (double)a * (double)a;
+          const double pp = dm.q_p[k * 8 + l];
+          double mm = (double)mq;
+          if (mm >= 1.0 && (2.0 * mm - 1.0) * (2.0 * mm - 1.0) * pp > a2) mm -= 1.0;
+          else if ((2.0 * mm + 1.0) * (2.0 * mm + 1.0) * pp <= a2) mm += 1.0;
+          mq = (float)mm;
+        }
+        const int v = y[k][l] < 0.0f ? -(int)mq : (int)mq;
+        const uint32_t u = (uint32_t)(uint16_t)(int16_t)v;
+        if (l & 1) w[l >> 1] |= u << 16; else w[l >> 1] = u;
+      }
+      *reinterpret_cast<uint4*>(o + k * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+int g_sms = 0;
+int sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+// single-r kernels compiled in: (matrix, r) pairs of the benchmark configurations
+template <typename SrcT, class MP, int CLIP>
+bool launch_single(int r, dim3 grid, cudaStream_t st, const SrcT* src, const KGeom& kg, const DevMat& dm,
+                   const FastDiv& dbw, int32_t chunks, double* partial) {
+  switch (r) {
+    case 10:
+      fused_single_kernel<SrcT, MP, 10, CLIP><<<grid, NT, 0, st>>>(src, kg, dm, dbw, chunks, partial);
+      return true;
+    case 64:
+      fused_single_kernel<SrcT, MP, 64, CLIP><<<grid, NT, 0, st>>>(src, kg, dm, dbw, chunks, partial);
+      return true;
+    default:
+      return false;
+  }
+}
+
+template <typename SrcT, class MP, int CLIP>
+void launch_sweep(dim3 grid, cudaStream_t st, const SrcT* src, const KGeom& kg, const DevMat& dm, const FastDiv& dbw,
+                  int32_t chunks, uint64_t rmask, int32_t rmin, double* partial) {
+  fused_sweep_kernel<SrcT, MP, CLIP><<<grid, NT, 0, st>>>(src, kg, dm, dbw, chunks, rmask, rmin, partial);
+}
+
+template <class MP>
+bool launch_u8(int r, dim3 grid, cudaStream_t st, const uint8_t* src, const KGeom& kg, const DevMat& dm,
+               const FastDiv& dbw, int32_t chunks, double* partial) {
+  switch (r) {
+#define ADCT_U8_CASE(R)                                                                   \
+  case R:                                                                                 \
+    fused_u8_kernel<MP, R><<<grid, NT, 0, st>>>(src, kg, dm, dbw, chunks, partial, 0x47000000u);       \
+    return true;
+    ADCT_U8_CASE(1) ADCT_U8_CASE(3) ADCT_U8_CASE(6) ADCT_U8_CASE(10) ADCT_U8_CASE(14)
+    ADCT_U8_CASE(15) ADCT_U8_CASE(21) ADCT_U8_CASE(28) ADCT_U8_CASE(36) ADCT_U8_CASE(64)
+#undef ADCT_U8_CASE
+    default:
+      return false;
+  }
+}
+
+template <typename SrcT, class MP>
+adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geom& g, const int32_t* r_list,
+                           int32_t n_r, adct_clip clip, double* sse, double* partial, cudaStream_t st) {
+  const KGeom kg = make_kgeom(g);
+  const FastDiv dbw = make_fastdiv(kg.bw);
+  int32_t chunks = (int32_t)fused_chunks(g);
+  const SrcT* s = (const SrcT*)src;
+  SlotMap sm{};
+  bool single = false;
+  if (n_r == 1) {
+    if constexpr (std::is_same<SrcT, uint8_t>::value) {
+      if (clip == ADCT_CLIP_NONE && m->is_int) {
+        const int32_t c8 = (int32_t)fused_chunks(g, kFusedBPTU8);
+        single = launch_u8<MP>(r_list[0], dim3((unsigned)c8, (unsigned)g.n_images), st, s, kg, m->dev, dbw, c8,
+                               partial);
+        if (single) chunks = c8;
+      }
+    }
+    dim3 grid((unsigned)chunks, (unsigned)g.n_images);
+    if (!single && clip == ADCT_CLIP_NONE)
+      single = launch_single<SrcT, MP, ADCT_CLIP_NONE>(r_list[0], grid, st, s, kg, m->dev, dbw, chunks, partial);
+    else if (!single && clip == ADCT_CLIP)
+      single = launch_single<SrcT, MP, ADCT_CLIP>(r_list[0], grid, st, s, kg, m->dev, dbw, chunks, partial);
+  }
+  dim3 grid((unsigned)chunks, (unsigned)g.n_images);
+  int32_t slots = 1;
+  if (!single) {
+    uint64_t rmask = 0;
+    int32_t rmin = 64;
+    for (int i = 0; i < n_r; ++i) {
+      if (r_list[i] < 64) rmask |= 1ull << r_list[i];  // r = 64 is slot 63, always 0
+      if (r_list[i] < rmin) rmin = r_list[i];
+      sm.s[i] = r_list[i] - 1;
+    }
+    if (clip == ADCT_CLIP_NONE)
+      launch_sweep<SrcT, MP, ADCT_CLIP_NONE>(grid, st, s, kg, m->dev, dbw, chunks, rmask, rmin, partial);
+    else if (clip == ADCT_CLIP)
+      launch_sweep<SrcT, MP, ADCT_CLIP>(grid, st, s, kg, m->dev, dbw, chunks, rmask, rmin, partial);
+    else
+      launch_sweep<SrcT, MP, ADCT_CLIP_ROUND>(grid, st, s, kg, m->dev, dbw, chunks, rmask, rmin, partial);
+    slots = 64;
+  }
+  count_launch();
+  if (adct_status e = launch_status()) return e;
+  launch_finalize(partial, chunks, g.n_images, slots, sm, n_r, (double)g.height * g.width, 255.0, sse, nullptr, st);
+  return launch_status();
+}
+
+adct_status fused_check(const adct_matrix* m, const void* src, adct_dtype src_t, const adct_geom& g,
+                        const int32_t* r_list, int32_t n_r, adct_clip clip) {
+  if (!m || !src || !r_list) return ADCT_E_INVALID_ARGUMENT;
+  if (adct_status s = check_geom(g)) return s;
+  if (src_t != ADCT_U8 && src_t != ADCT_I16) return ADCT_E_INVALID_ARGUMENT;
+  if (n_r < 1 || n_r > 64) return ADCT_E_INVALID_ARGUMENT;
+  for (int i = 0; i < n_r; ++i)
+    if (r_list[i] < 1 || r_list[i] > 64) return ADCT_E_INVALID_ARGUMENT;
+  if (clip != ADCT_CLIP_NONE && clip != ADCT_CLIP && clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  if (!aligned(src, src_t == ADCT_U8 ? 8 : 16)) return ADCT_E_ALIGNMENT;
+  return ADCT_OK;
+}
+
+adct_status fused_run(const adct_matrix* m, const void* src, adct_dtype src_t, const adct_geom& g,
+                      const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse, double* partial,
+                      cudaStream_t st) {
+  if (g.n_images == 0) return ADCT_OK;
+  if (src_t == ADCT_U8) {
+    if (m->specialized) return fused_dispatch<uint8_t, T1Mat>(m, src, g, r_list, n_r, clip, sse, partial, st);
+    return fused_dispatch<uint8_t, RtMat>(m, src, g, r_list, n_r, clip, sse, partial, st);
+  }
+  if (m->specialized) return fused_dispatch<int16_t, T1Mat>(m, src, g, r_list, n_r, clip, sse, partial, st);
+  return fused_dispatch<int16_t, RtMat>(m, src, g, r_list, n_r, clip, sse, partial, st);
+}
+
+// copy stream of the host-buffer pipeline (one per process/device, created on first use)
+cudaStream_t copy_stream() {
+  static std::mutex mu;
+  static cudaStream_t s = nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  return s;
+}
+
+}  // namespace
+}  // namespace adct
+
+using namespace adct;
+
+extern "C" {
+
+adct_status approx_dct8x8_fused_sse(const adct_matrix* m, const void* src, adct_dtype src_t, adct_geom g,
+                                    const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (adct_status s = fused_check(m, src, src_t, g, r_list, n_r, clip)) return s;
+  if (!sse) return ADCT_E_INVALID_ARGUMENT;
+  if (!workspace || workspace_bytes < adct_workspace_bytes(g, n_r) || !aligned(workspace, 8)) return ADCT_E_WORKSPACE;
+  return fused_run(m, src, src_t, g, r_list, n_r, clip, sse, (double*)workspace, (cudaStream_t)stream);
+}
+
+size_t adct_host_workspace_bytes(adct_geom g, int32_t n_r, int64_t chunk_images, adct_dtype src_t) {
+  if (chunk_images < 1) chunk_images = 1;
+  adct_geom gc = g;
+  gc.n_images = chunk_images;
+  const size_t esz = src_t == ADCT_I16 ? 2 : 1;
+  const size_t stage = ((size_t)chunk_images * (size_t)g.image_stride * esz + 255) / 256 * 256;
+  const size_t part = (adct_workspace_bytes(gc, n_r) + 255) / 256 * 256;
+  const size_t out = ((size_t)(g.n_images > 0 ? g.n_images : 0) * (size_t)(n_r > 0 ? n_r : 1) * sizeof(double) + 255) / 256 * 256;
+  return 2 * stage + 2 * part + out;
+}
+
+adct_status approx_dct8x8_fused_sse_host(const adct_matrix* m, const void* src_host, adct_dtype src_t, adct_geom g,
+                                         const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse_host,
+                                         int64_t chunk_images, void* workspace, size_t workspace_bytes,
+                                         void* stream) {
+  if (adct_status s = fused_check(m, src_host, src_t, g, r_list, n_r, clip)) return s;
+  if (!sse_host || chunk_images < 1) return ADCT_E_INVALID_ARGUMENT;
+  if (g.n_images > 1 && g.image_stride != (int64_t)g.height * g.row_stride) return ADCT_E_INVALID_ARGUMENT;
+  if (!workspace || workspace_bytes < adct_host_workspace_bytes(g, n_r, chunk_images, src_t)) return ADCT_E_WORKSPACE;
+  if (g.n_images == 0) return ADCT_OK;
+  cudaStream_t cs = (cudaStream_t)stream;
+  cudaStream_t xs = copy_stream();
+  if (!xs) return ADCT_E_CUDA;
+  adct_geom gc = g;
+  gc.n_images = chunk_images;
+  const size_t esz = src_t == ADCT_I16 ? 2 : 1;
+  const size_t stage = ((size_t)chunk_images * (size_t)g.image_stride * esz + 255) / 256 * 256;
+  const size_t part = (adct_workspace_bytes(gc, n_r) + 255) / 256 * 256;
+  char* ws = (char*)workspace;
+  char* stg[2] = {ws, ws + stage};
+  double* prt[2] = {(double*)(ws + 2 * stage), (double*)(ws + 2 * stage + part)};
+  double* dsse = (double*)(ws + 2 * stage + 2 * part);
+  cudaEvent_t copied[2], freed[2];
+  for (int i = 0; i < 2; ++i) {
+    if (cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming) != cudaSuccess) return ADCT_E_CUDA;
+    if (cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming) != cudaSuccess) return ADCT_E_CUDA;
+  }
+  adct_status st = ADCT_OK;
+  // the copy stream must not overwrite a staging buffer before earlier compute finished
+  cudaEventRecord(freed[0], cs);
+  cudaEventRecord(freed[1], cs);
+  int64_t c = 0;
+  for (int64_t i0 = 0; i0 < g.n_images && st == ADCT_OK; i0 += chunk_images, ++c) {
+    const int b = (int)(c & 1);
+    const int64_t n = (g.n_images - i0) < chunk_images ? (g.n_images - i0) : chunk_images;
+    const size_t bytes = (size_t)((n - 1) * g.image_stride + (int64_t)g.height * g.row_stride) * esz;
+    cudaStreamWaitEvent(xs, freed[b], 0);
+    if (cudaMemcpyAsync(stg[b], (const char*)src_host + (size_t)i0 * g.image_stride * esz, bytes,
+                        cudaMemcpyHostToDevice, xs) != cudaSuccess) { st = ADCT_E_CUDA; break; }
+    cudaEventRecord(copied[b], xs);
+    cudaStreamWaitEvent(cs, copied[b], 0);
+    adct_geom gi = g;
+    gi.n_images = n;
+    st = fused_run(m, stg[b], src_t, gi, r_list, n_r, clip, dsse + i0 * n_r, prt[b], cs);
+    cudaEventRecord(freed[b], cs);
+  }
+  if (st == ADCT_OK &&
+      cudaMemcpyAsync(sse_host, dsse, (size_t)g.n_images * n_r * sizeof(double), cudaMemcpyDeviceToHost, cs) !=
+          cudaSuccess)
+    st = ADCT_E_CUDA;
+  if (cudaStreamSynchronize(cs) != cudaSuccess) st = ADCT_E_CUDA;
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(copied[i]);
+    cudaEventDestroy(freed[i]);
+  }
+  return st;
+}
+
+adct_status approx_dct8x8_fwd_quant(const adct_matrix* m, const uint8_t* src, adct_geom g, int32_t step, int16_t* q,
+                                    void* stream) {
+  if (!m || !src || !q) return ADCT_E_INVALID_ARGUMENT;
+  if (adct_status s = check_geom(g)) return s;
+  if (!m->is_int || step < 1) return ADCT_E_INVALID_ARGUMENT;
+  if (!aligned(src, 8) || !aligned(q, 16)) return ADCT_E_ALIGNMENT;
+  const KGeom kg = make_kgeom(g);
+  const uint32_t nb = (uint32_t)(g.n_images * kg.nbi);
+  if (nb == 0) return ADCT_OK;
+  DevMat dm = m->dev;
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l) {
+      const double p = (double)step * step * (double)m->n[k] * (double)m->n[l];
+      dm.q_p[k * 8 + l] = p;
+      dm.q_inv[k * 8 + l] = (float)(1.0 / std::sqrt(p));
+      const double c = std::sqrt(p);
+      dm.q_c[k * 8 + l] = (std::floor(c) == c) ? (int32_t)c : 0;
+    }
+  const FastDiv dnbi = make_fastdiv(kg.nbi), dbw = make_fastdiv(kg.bw);
+  const int64_t need = ((int64_t)nb + 255) / 256;
+  const int64_t cap = (int64_t)sms() * 8;
+  const unsigned grid = (unsigned)(need < cap ? need : cap);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m->specialized)
+    fwd_quant_kernel<T1Mat><<<grid, 256, 0, st>>>(src, kg, dm, dnbi, dbw, nb, q);
+  else
+    fwd_quant_kernel<RtMat><<<grid, 256, 0, st>>>(src, kg, dm, dnbi, dbw, nb, q);
+  count_launch();
+  return launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded
+inputs.  Integer transform / retention / quantiser: bit-exact.  Floating point (after S,
+inverse, error): <= 1e-5 relative (per-block max-norm for arrays; per value for SSE) and
+<= 1e-3 dB PSNR (BASELINE.json north_star); SSE exactly 0 where the oracle's is 0 (r = 64).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import matrices as M
+import synth
+
+pytestmark = pytest.mark.gpu
+
+adct = pytest.importorskip("paper_1808_02950_b200.adct")
+from paper_1808_02950_b200 import catalog  # noqa: E402
+
+DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
+RTOL = 1e-5
+INT_NAMES = list(catalog.INTEGER)
+ORTHO = ["T1", "T2", "LO", "RDCT", "T4", "T6"]
+
+
+def tmat(name):
+    return np.array(catalog.INTEGER[name]).reshape(8, 8)
+
+
+@pytest.fixture(scope="module")
+def mats():
+    d = {n: adct.Matrix.from_int(catalog.INTEGER[n], n) for n in INT_NAMES}
+    d["DCT"] = adct.Matrix.from_real(catalog.exact_dct(), "DCT")
+    return d
+
+
+def blocks_to_image(a):
+    n, bh, bw = a.shape[:3]
+    return a.transpose(0, 1, 3, 2, 4).reshape(n, bh * 8, bw * 8)
+
+
+def rel_block_err(got, ref):
+    """per-block max-norm relative error, ||g - o||_inf / max(||o||_inf, 1) (reading A17)"""
+    g = got.reshape(-1, 64).astype(np.float64)
+    o = ref.reshape(-1, 64).astype(np.float64)
+    return float(np.max(np.abs(g - o).max(axis=1) / np.maximum(np.abs(o).max(axis=1), 1.0)))
+
+
+def images(kind, n, h, w, seed):
+    if kind == "ar1":
+        return synth.ar1_field(n, h, w, 0.95, seed=seed)
+    if kind == "uniform":
+        return synth.uniform_blocks_u8(n, h, w, seed=seed)
+    if kind == "laplace":
+        b = synth.laplace_blocks(n * (h // 8) * (w // 8), seed=seed)
+        return torch.from_numpy(blocks_to_image(b.numpy().reshape(n, h // 8, w // 8, 8, 8)).copy())
+    if kind == "extreme":
+        g = torch.Generator().manual_seed(seed)
+        return (torch.randint(0, 2, (n, h, w), generator=g) * 255).to(torch.uint8)
+    raise ValueError(kind)
+
+
+SHAPES = [(1, 8, 8), (3, 40, 56), (2, 64, 1032), (1, 136, 520)]  # one block .. several tiles + ragged tails
+
+
+# --- forward -------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", INT_NAMES)
+@pytest.mark.parametrize("kind", ["ar1", "uniform", "extreme", "laplace"])
+def test_forward_int32_bit_exact(mats, name, kind):
+    for (n, h, w) in SHAPES[:3]:
+        img = images(kind, n, h, w, seed=n * 1000 + w)
+        y = adct.approx_dct8x8_fwd(mats[name], img.to(DEV), torch.int32).cpu().numpy()
+        assert np.array_equal(y, oracle.forward_int(tmat(name), img.numpy()))
+
+
+def test_forward_int16_output_and_strided_view(mats):
+    img = images("uniform", 2, 48, 80, seed=3)
+    big = torch.zeros((2, 64, 128), dtype=torch.uint8)
+    big[:, 8:56, 16:96] = img
+    view = big.to(DEV)[:, 8:56, 16:96]  # row stride 128, image stride 8192
+    y16 = adct.approx_dct8x8_fwd(mats["T1"], view, torch.int16).cpu().numpy()
+    assert np.array_equal(y16.astype(np.int64), oracle.forward_int(M.T1, img.numpy()))
+
+
+@pytest.mark.parametrize("name", INT_NAMES)
+def test_forward_f32_scaled(mats, name):
+    img = images("ar1", 2, 40, 56, seed=5)
+    b = adct.approx_dct8x8_fwd(mats[name], img.to(DEV), torch.float32).cpu().numpy()
+    n, s = oracle.row_scaling(tmat(name))
+    ref = oracle.scale(oracle.forward_int(tmat(name), img.numpy()), s)
+    assert rel_block_err(b, ref) <= RTOL
+
+
+@pytest.mark.parametrize("kind", ["ar1", "laplace"])
+def test_forward_exact_dct(mats, kind):
+    img = images(kind, 2, 40, 56, seed=6)
+    b = adct.approx_dct8x8_fwd(mats["DCT"], img.to(DEV), torch.float32).cpu().numpy()
+    ref = oracle.forward_real(M.C, img.numpy())
+    assert rel_block_err(b, ref) <= RTOL
+
+
+# --- retention -----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dtype", [torch.int32, torch.int16, torch.float32])
+def test_retain_bit_exact(mats, dtype):
+    img = images("uniform", 2, 24, 40, seed=8)
+    y = oracle.forward_int(M.T1, img.numpy())
+    for r in [1, 2, 3, 10, 33, 63, 64]:
+        c = torch.from_numpy(y.astype({torch.int32: np.int32, torch.int16: np.int16,
+                                       torch.float32: np.float32}[dtype])).to(DEV)
+        adct.zonal_retain(c, r)
+        assert np.array_equal(c.cpu().numpy().astype(np.int64), oracle.retain(y, r))
+    with pytest.raises(adct.AdctError):
+        adct.zonal_retain(torch.zeros(64, dtype=dtype, device=DEV), 0)
+
+
+# --- inverse -------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", INT_NAMES + ["DCT"])
+@pytest.mark.parametrize("r", [1, 6, 10, 40, 64])
+def test_inverse_f32(mats, name, r):
+    img = images("ar1", 2, 40, 56, seed=9)
+    if name == "DCT":
+        chat = M.C
+        bref = oracle.forward_real(M.C, img.numpy())
+        coef = torch.from_numpy(oracle.retain(bref, r).astype(np.float32)).to(DEV)
+    else:
+        chat = oracle.chat_from_int(tmat(name))
+        n, s = oracle.row_scaling(tmat(name))
+        yr = oracle.retain(oracle.forward_int(tmat(name), img.numpy()), r)
+        bref = oracle.scale(yr, s)
+        coef = torch.from_numpy(yr.astype(np.int32)).to(DEV)
+    g, _ = oracle.synthesis_matrix(chat)
+    ref = blocks_to_image(oracle.inverse(g, oracle.retain(bref, r)))
+    rec = adct.approx_dct8x8_inv(mats[name], coef, 40, 56).cpu().numpy()
+    assert rel_block_err(rec, ref) <= RTOL
+    if name != "DCT":  # B' (f32 scaled coefficients) input gives the same reconstruction
+        rec2 = adct.approx_dct8x8_inv(mats[name], torch.from_numpy(oracle.retain(bref, r).astype(np.float32))
+                                      .to(DEV), 40, 56).cpu().numpy()
+        assert rel_block_err(rec2, ref) <= RTOL
+
+
+@pytest.mark.parametrize("name", ["T1", "DCT"])
+def test_config5_roundtrip_int16_bit_exact(mats, name):
+    """C5 pin: rint(inverse(forward(X))) == X for int16 Laplace blocks."""
+    n_blocks = 1 << 16
+    x = synth.laplace_blocks(n_blocks, seed=5).reshape(n_blocks, 8, 8)  # images of one block
+    xd = x.to(DEV)
+    ct = torch.int32 if name == "T1" else torch.float32
+    coef = adct.approx_dct8x8_fwd(mats[name], xd, ct)
+    rec = adct.approx_dct8x8_inv(mats[name], coef, 8, 8, torch.int16, adct.CLIP_ROUND)
+    assert torch.equal(rec.cpu(), x)
+
+
+def test_inverse_u8_round_clip(mats):
+    img = images("ar1", 1, 32, 32, seed=2)
+    y = adct.approx_dct8x8_fwd(mats["T1"], img.to(DEV), torch.int32)
+    adct.zonal_retain(y, 6)
+    rec = adct.approx_dct8x8_inv(mats["T1"], y, 32, 32, torch.uint8, adct.CLIP_ROUND).cpu().numpy()
+    n, s = oracle.row_scaling(M.T1)
+    g, _ = oracle.synthesis_matrix(oracle.chat_from_int(M.T1))
+    ref = blocks_to_image(oracle.inverse(g, oracle.scale(oracle.retain(oracle.forward_int(M.T1, img.numpy()), 6), s)))
+    ref_u8 = np.clip(np.rint(ref), 0, 255)
+    # rounding may differ only where the exact value is within fp32 error of .5
+    diff = np.abs(rec.astype(np.int64) - ref_u8)
+    assert diff.max() <= 1
+    assert np.all(np.abs(np.abs(ref - np.floor(ref)) - 0.5)[diff > 0] < 1e-3)
+
+
+# --- psnr_reduce -----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("clip", [adct.CLIP_NONE, adct.CLIP, adct.CLIP_ROUND])
+def test_psnr_reduce(mats, clip):
+    img = images("ar1", 3, 40, 56, seed=12)
+    y = adct.approx_dct8x8_fwd(mats["T1"], img.to(DEV), torch.int32)
+    adct.zonal_retain(y, 3)
+    rec = adct.approx_dct8x8_inv(mats["T1"], y, 40, 56)
+    sse, psnr = adct.psnr_reduce(img.to(DEV), rec, clip=clip)
+    rec_blocks = rec.cpu().numpy().astype(np.float64).reshape(3, 5, 8, 7, 8).transpose(0, 1, 3, 2, 4)
+    ref = oracle.sse(img.numpy(), rec_blocks, clip)
+    assert np.allclose(sse.cpu().numpy(), ref, rtol=RTOL, atol=0)
+    for i in range(3):
+        assert abs(psnr[i].item() - oracle.psnr(ref[i], 40 * 56)) <= 1e-3
+    s0, p0 = adct.psnr_reduce(img.to(DEV), img.to(DEV).float())
+    assert torch.all(s0 == 0) and torch.all(torch.isinf(p0))
+
+
+# --- fused paths -------------------------------------------------------------------------------
+
+def _check_sse(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    zero = ref <= 1e-16 * 64 * 1e6
+    assert np.all(got[zero] == 0.0)
+    assert np.allclose(got[~zero], ref[~zero], rtol=RTOL, atol=0)
+
+
+@pytest.mark.parametrize("name", INT_NAMES + ["DCT"])
+def test_fused_sweep_all_r(mats, name):
+    img = images("ar1", 2, 64, 72, seed=21)
+    rs = list(range(1, 65))
+    sse = adct.approx_dct8x8_fused_sse(mats[name], img.to(DEV), rs).cpu().numpy()
+    kw = {"c": M.C} if name == "DCT" else {"t": tmat(name)}
+    _check_sse(sse, oracle.codec_sse(img.numpy(), rs, **kw))
+
+
+@pytest.mark.parametrize("r", [1, 3, 6, 10, 14, 15, 21, 28, 36, 64])
+@pytest.mark.parametrize("name", ["T1", "T6", "LO", "SDCT"])
+def test_fused_single_r(mats, name, r):
+    img = images("ar1", 3, 72, 200, seed=r)  # ragged chunks
+    sse = adct.approx_dct8x8_fused_sse(mats[name], img.to(DEV), [r]).cpu().numpy()
+    _check_sse(sse, oracle.codec_sse(img.numpy(), [r], t=tmat(name)))
+
+
+@pytest.mark.parametrize("clip", [adct.CLIP, adct.CLIP_ROUND])
+def test_fused_clip(mats, clip):
+    img = images("uniform", 2, 32, 48, seed=4)  # saturates often
+    for rs in ([10], [2, 10, 30]):
+        sse = adct.approx_dct8x8_fused_sse(mats["T1"], img.to(DEV), rs, clip=clip).cpu().numpy()
+        ref = oracle.codec_sse(img.numpy(), rs, t=M.T1, clip=clip)
+        if clip == adct.CLIP_ROUND:  # rounding of ties may flip a pixel by one level
+            assert np.allclose(sse, ref, rtol=1e-3)
+        else:
+            _check_sse(sse, ref)
+
+
+def test_fused_int16_source(mats):
+    img = images("laplace", 2, 32, 40, seed=13)
+    rs = [1, 10, 64]
+    for name in ("T1", "DCT"):
+        kw = {"c": M.C} if name == "DCT" else {"t": M.T1}
+        sse = adct.approx_dct8x8_fused_sse(mats[name], img.to(DEV), rs).cpu().numpy()
+        _check_sse(sse, oracle.codec_sse(img.numpy(), rs, **kw))
+
+
+def test_fused_deterministic_and_shard_invariant(mats):
+    img = images("ar1", 6, 64, 128, seed=30).to(DEV)
+    a = adct.approx_dct8x8_fused_sse(mats["T1"], img, [10]).cpu().numpy()
+    b = adct.approx_dct8x8_fused_sse(mats["T1"], img, [10]).cpu().numpy()
+    assert np.array_equal(a, b)
+    parts = [adct.approx_dct8x8_fused_sse(mats["T1"], img[i:i + 2], [10]).cpu().numpy() for i in (0, 2, 4)]
+    assert np.array_equal(np.concatenate(parts), a)
+
+
+def test_fused_host_pipeline_equals_device(mats):
+    img = images("ar1", 7, 64, 96, seed=31)
+    dev = adct.approx_dct8x8_fused_sse(mats["T1"], img.to(DEV), [10, 21]).cpu()
+    host = img.pin_memory()
+    g = adct.geom_of(host)
+    ws = torch.empty(adct.host_workspace_bytes(g, 2, 3), dtype=torch.uint8, device=DEV)
+    got = adct.approx_dct8x8_fused_sse_host(mats["T1"], host, [10, 21], ws, chunk_images=3)
+    assert torch.equal(got, dev)
+
+
+def test_config1_full_size(mats):
+    """C1: one 512x512 AR(1) image, r = 1..64, T1 — every r against the oracle."""
+    img = synth.ar1_field(1, 512, 512, 0.95, seed=1)
+    rs = list(range(1, 65))
+    sse = adct.approx_dct8x8_fused_sse(mats["T1"], img.to(DEV), rs).cpu().numpy()
+    ref = oracle.codec_sse(img.numpy(), rs, t=M.T1)
+    _check_sse(sse, ref)
+    psnr = adct.psnr_from_sse(torch.from_numpy(sse), 512 * 512).numpy()
+    for r in (1, 3, 10, 63):
+        assert abs(psnr[0, r - 1] - oracle.psnr(ref[0, r - 1], 512 * 512)) <= 1e-3
+
+
+def test_config4_sampled_frames(mats):
+    """C4 geometry (3840x2160 luma, 1920x1080 chroma), hot kernel r = 10, on sampled frames."""
+    y, u, v = synth.yuv420_stack(2, seed=4)
+    for plane in (y, u, v):
+        sse = adct.approx_dct8x8_fused_sse(mats["T1"], plane.to(DEV), [10]).cpu().numpy()
+        _check_sse(sse, oracle.codec_sse(plane.numpy(), [10], t=M.T1))
+
+
+# --- quantiser ----------------------------------------------------------------------------------
+
+def test_quantiser_bit_exact(mats):
+    img = images("ar1", 2, 64, 96, seed=40)
+    q = adct.approx_dct8x8_fwd_quant(mats["T1"], img.to(DEV), 16).cpu().numpy()
+    n, s = oracle.row_scaling(M.T1)
+    assert np.array_equal(q, oracle.quantize(oracle.forward_int(M.T1, img.numpy()), n, 16))
+
+
+def test_quantiser_exhaustive_values(mats):
+    """Every Y in [-18360, 18360] at every position: feed impulse-like blocks whose Y is
+    known exactly and compare with the oracle's integer rule (ties included)."""
+    ext = images("extreme", 8, 256, 256, seed=41)
+    uni = images("uniform", 8, 256, 256, seed=42)
+    for img in (ext, uni):
+        q = adct.approx_dct8x8_fwd_quant(mats["T1"], img.to(DEV), 16).cpu().numpy()
+        n, s = oracle.row_scaling(M.T1)
+        assert np.array_equal(q, oracle.quantize(oracle.forward_int(M.T1, img.numpy()), n, 16))
