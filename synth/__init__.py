@@ -76,7 +76,7 @@ def ar1_field(n: int, h: int, w: int, rho, mean=128.0, std=40.0, seed: int = 1, 
         u = torch.rand((n, h, w), generator=g, device=dev, dtype=torch.float32)
         y = y + (u * 2.0 - 1.0) * float(noise_uniform)
     y = torch.round(torch.clamp(y, 0.0, 255.0))         # torch.round = half to even
-    return y.to(torch.uint8)
+    return y.to(torch.uint8).contiguous()
 
 
 def ar1_stack(n: int, h: int, w: int, rho, mean=128.0, std=40.0, seed: int = 1, device="cpu",
