@@ -73,4 +73,104 @@ inline int64_t fused_chunks(const adct_geom& g, int bpt = kFusedBPT) {
 constexpr int kSseRows = 8;  // image rows per CTA in psnr_reduce
 inline int64_t sse_chunks(const adct_geom& g) { return (g.height + kSseRows - 1) / kSseRows; }
 
+// ---- streaming (bulk-copy staged) fused kernel: stage plan ------------------------------------
+// A "band" is the 8 image rows of one block row.  A stage is G consecutive bands of ONE image,
+// copied global -> shared memory with cp.async.bulk and consumed by kStreamConsumers threads,
+// one 8x8 block per thread per pass.  Per-(stage, consumer warp) fp64 partials make the
+// per-image sums independent of the grid (and of how images are sharded over GPUs).
+constexpr int kStreamWarps = 16;                    // 1 producer warp + 15 consumer warps
+constexpr int kStreamThreads = 32 * kStreamWarps;
+constexpr int kStreamConsumerWarps = kStreamWarps - 1;
+constexpr int kStreamConsumers = 32 * kStreamConsumerWarps;  // 480
+constexpr int64_t kStreamSmemBudget = 200 * 1024;   // stage ring (of 227 KB per CTA)
+constexpr int64_t kStreamStageTargetDefault = 32 * 1024;
+// stage-size target in bytes (env ADCT_STREAM_STAGE_KB overrides, for tuning runs)
+int64_t stream_stage_target();
+constexpr int32_t kStreamChunkStages = 8;           // stages per partial-sum chunk
+
+struct StreamPlan {
+  int32_t G;            // bands per stage
+  int32_t G0;           // bands per "group" of one block per consumer (0: no fixed mapping)
+  int32_t spi;          // stages per image
+  int32_t cpi;          // chunks per image (kStreamChunkStages stages each, the last partial)
+  int32_t stages_in_ring;
+  int64_t stage_bytes;  // G * 8 * W (bytes of one full stage)
+  int64_t n_chunks;     // n_images * cpi
+  bool ok;              // geometry supported by the streaming kernel
+};
+
+inline StreamPlan stream_plan(const adct_geom& g, int esz = 1) {
+  StreamPlan p{};
+  const int64_t W = (int64_t)g.width * esz, bw = g.width / 8, bh = g.height / 8;
+  if (bw <= 0 || bh <= 0) return p;
+  int64_t G;
+  if (kStreamConsumers % bw == 0) {
+    p.G0 = (int32_t)(kStreamConsumers / bw);  // one block per consumer thread per group
+    int64_t k = stream_stage_target() / (p.G0 * 8 * W);
+    if (k < 1) k = 1;
+    G = p.G0 * k;
+  } else {
+    G = stream_stage_target() / (8 * W);
+    if (G < 1) G = 1;
+  }
+  if (G > bh) G = bh;
+  p.G = (int32_t)G;
+  p.spi = (int32_t)((bh + G - 1) / G);
+  p.cpi = (p.spi + kStreamChunkStages - 1) / kStreamChunkStages;
+  p.stage_bytes = G * 8 * W;
+  p.stages_in_ring = (int32_t)(kStreamSmemBudget / p.stage_bytes);
+  if (p.stages_in_ring > 8) p.stages_in_ring = 8;
+  p.n_chunks = g.n_images * (int64_t)p.cpi;
+  // bulk copies move 16-byte multiples between 16-byte aligned addresses; the mbarrier
+  // transaction count of one stage must stay below 2^20
+  p.ok = p.stages_in_ring >= 2 && (W % 16) == 0 && ((int64_t)g.row_stride * esz) % 16 == 0 &&
+         ((int64_t)g.image_stride * esz) % 16 == 0 && p.stage_bytes < (1 << 20) &&
+         p.n_chunks < ((int64_t)1 << 31);
+  return p;
+}
+// ---- warp-tile streaming kernel (the default hot kernel) ---------------------------------------
+// Every warp owns a private ring of kWtSlots tiles.  A tile is 16 image rows x 256 bytes (two
+// bands of 32 horizontally adjacent 8x8 blocks: 2 blocks per lane), fetched by ONE TMA tensor
+// copy (cp.async.bulk.tensor.3d over a {W, H, n_images} uint8 tensor map, box {256, 16, 1};
+// out-of-range parts are zero-filled, and an all-zero block has exactly zero error) that
+// completes on the warp's own mbarrier.  No producer warp and no cross-warp barrier: each warp
+// refills the slot it just consumed.  A chunk is kWtChunkTiles consecutive tiles of one image;
+// per-(chunk, warp) fp64 partials keep the per-image sums independent of the grid.
+constexpr int kWtWarps = 16;
+constexpr int kWtThreads = 32 * kWtWarps;
+constexpr int kWtSlots = 3;
+constexpr int kWtSlice = 256;                       // bytes of a row slice = 32 blocks
+constexpr int kWtRows = 16;                         // image rows per tile (2 bands)
+constexpr int kWtTileBytes = kWtRows * kWtSlice;
+constexpr int kWtChunkTiles = kWtWarps * 8;         // 8 tiles per warp per chunk
+constexpr size_t kWtSmem = (size_t)kWtWarps * kWtSlots * kWtTileBytes + (size_t)kWtWarps * kWtSlots * 8 + 128;
+
+struct WtPlan {
+  int32_t tpb;      // tiles per band pair (ceil(W / 256))
+  int32_t tpi;      // tiles per image
+  int32_t cpi;      // chunks per image
+  int64_t n_chunks;
+  bool ok;
+};
+inline WtPlan wt_plan(const adct_geom& g) {
+  WtPlan p{};
+  const int64_t W = g.width, H = g.height;
+  if (W <= 0 || H <= 0) return p;
+  p.tpb = (int32_t)((W + kWtSlice - 1) / kWtSlice);
+  p.tpi = (int32_t)(((H + kWtRows - 1) / kWtRows) * p.tpb);
+  p.cpi = (p.tpi + kWtChunkTiles - 1) / kWtChunkTiles;
+  p.n_chunks = g.n_images * (int64_t)p.cpi;
+  // tensor-map constraints: 16-byte aligned strides (< 2^40), dimensions < 2^32
+  p.ok = (g.row_stride % 16) == 0 && (g.image_stride % 16) == 0 && g.image_stride < ((int64_t)1 << 40) &&
+         p.n_chunks < ((int64_t)1 << 31);
+  return p;
+}
+
+inline int64_t stream_partials_per_image(const adct_geom& g) {
+  const StreamPlan p = stream_plan(g);
+  const WtPlan w = wt_plan(g);
+  const int64_t a = (int64_t)p.cpi * kStreamConsumerWarps, b = (int64_t)w.cpi * kWtWarps;
+  return a > b ? a : b;
+}
+
 }  // namespace adct

@@ -208,20 +208,34 @@ __global__ void __launch_bounds__(kRedNT) sse_kernel(const OrigT* __restrict__ o
   if (threadIdx.x == 0) partial[(int64_t)img * chunks + blockIdx.x] = tot;
 }
 
-__global__ void finalize_kernel(const double* __restrict__ partial, int32_t chunks, int64_t n_images,
-                                int32_t slots, SlotMap slot_of, int32_t n_out,
-                                double npix, double peak, double* __restrict__ sse, double* __restrict__ psnr) {
-  // one thread per (image, output): sums the image's chunk partials in chunk order
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_images * n_out) return;
-  const int64_t img = t / n_out;
-  const int32_t o = (int32_t)(t - img * n_out);
+// one CTA per (image, output): thread t adds chunks t, t + 256, ... in order, then a fixed
+// shared-memory tree combines the 256 sums — deterministic, independent of the grid that
+// produced the partials.
+constexpr int kFinNT = 256;
+__global__ void __launch_bounds__(kFinNT) finalize_kernel(const double* __restrict__ partial, int32_t chunks,
+                                                          int64_t n_images, int32_t slots, SlotMap slot_of,
+                                                          int32_t n_out, double npix, double peak,
+                                                          double* __restrict__ sse, double* __restrict__ psnr) {
+  __shared__ double red[kFinNT];
+  const int64_t img = blockIdx.x;
+  const int32_t o = blockIdx.y;
   const int32_t s = slot_of.s[o];
   double acc = 0.0;
   if (s >= 0)
-    for (int32_t c = 0; c < chunks; ++c) acc += partial[((int64_t)img * chunks + c) * slots + s];
-  sse[t] = acc;
-  if (psnr) psnr[t] = acc == 0.0 ? INFINITY : 10.0 * log10(peak * peak / (acc / npix));
+    for (int32_t c = threadIdx.x; c < chunks; c += kFinNT) acc += partial[((int64_t)img * chunks + c) * slots + s];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+#pragma unroll
+  for (int w = kFinNT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double tot = red[0];
+    const int64_t t = img * n_out + o;
+    sse[t] = tot;
+    if (psnr) psnr[t] = tot == 0.0 ? INFINITY : 10.0 * log10(peak * peak / (tot / npix));
+  }
 }
 
 }  // namespace
@@ -229,10 +243,9 @@ __global__ void finalize_kernel(const double* __restrict__ partial, int32_t chun
 // exported to fused.cu
 void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
                      int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st) {
-  const int64_t n = n_images * n_out;
-  if (n == 0) return;
-  finalize_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(partial, chunks, n_images, slots, slot_of, n_out,
-                                                                npix, peak, sse, psnr);
+  if (n_images * n_out == 0) return;
+  finalize_kernel<<<dim3((unsigned)n_images, (unsigned)n_out), kFinNT, 0, st>>>(partial, chunks, n_images, slots,
+                                                                                slot_of, n_out, npix, peak, sse, psnr);
   count_launch();
 }
 

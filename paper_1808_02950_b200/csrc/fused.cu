@@ -8,43 +8,37 @@
 // Results therefore do not depend on scheduling, and sharding images over GPUs gives the
 // same per-image sums bit for bit.
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "adct_host.h"
+#include "fused_common.cuh"
 
 namespace adct {
 
 void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
                      int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st);
+void launch_sweep_any(bool u8, bool specialized, int clip, dim3 grid, cudaStream_t st, const void* src,
+                      const KGeom& kg, const DevMat& dm, const FastDiv& dbw, int32_t chunks, uint64_t rmask,
+                      int32_t rmin, double* partial);
+bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
+                     double* partial, cudaStream_t st, adct_status* status);
 
 namespace {
 
+// ADCT_DISABLE_STREAM=1 selects the register-prefetch kernels (A/B comparison and tests)
+const bool g_disable_stream = [] {
+  const char* e = std::getenv("ADCT_DISABLE_STREAM");
+  return e && e[0] == '1';
+}();
+
 constexpr int NT = kRedNT;
 constexpr int BPT = kFusedBPT;
-constexpr int BPT_U8 = kFusedBPTU8;
 
 __host__ __device__ constexpr int popc64(uint64_t v) {
   int c = 0;
   for (int i = 0; i < 64; ++i) c += (int)((v >> i) & 1u);
   return c;
-}
-
-template <int CLIP>
-__device__ __forceinline__ float clipv(float v, float lo, float hi) {
-  if (CLIP == ADCT_CLIP_NONE) return v;
-  v = fminf(fmaxf(v, lo), hi);
-  if (CLIP == ADCT_CLIP_ROUND) v = rintf(v);
-  return v;
-}
-
-template <typename SrcT>
-__device__ __forceinline__ void load_rows(const SrcT* __restrict__ base, const KGeom& g, const FastDiv& dbw,
-                                          uint32_t q, typename Src<SrcT>::Row (&r)[8]) {
-  const uint32_t by = fdiv(q, dbw);
-  const uint32_t bx = q - by * g.bw;
-  const SrcT* p = base + (int64_t)by * 8 * g.row_stride + (int64_t)bx * 8;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) r[i] = Src<SrcT>::load(p + (int64_t)i * g.row_stride);
 }
 
 // ---- single r, compile-time retention pattern ------------------------------------------
@@ -84,132 +78,6 @@ __device__ __forceinline__ float block_sse(const MP& m, const typename Src<SrcT>
   return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-// ---- the hot path: u8 samples, integer matrix, no clip ----------------------------------------
-// Samples are turned into fp32 with one PRMT each (bit pattern 0x4700xx00 = M + x, M = 2^15;
-// every intermediate stays an integer below 2^24, so the forward is still exact).  The vertical
-// butterflies s_i = x_i + x_{7-i}, t_i = x_i - x_{7-i} of the forward are kept and reused by
-// the error: with the inverse's last butterfly x_hat_i = E_i + O_i, x_hat_{7-i} = E_i - O_i,
-//   (x_i - x_hat_i)^2 + (x_{7-i} - x_hat_{7-i})^2 = ((s_i - 2E_i)^2 + (t_i - 2O_i)^2) / 2,
-// so each pixel pair costs two differences and two squares.  The weights carry the factor 2.
-__host__ __device__ constexpr uint32_t row_mask(uint64_t nz) {
-  uint32_t r = 0;
-  for (int k = 0; k < 8; ++k)
-    if ((nz >> (8 * k)) & 0xffull) r |= 1u << k;
-  return r;
-}
-
-// the selector is an immediate and the magic 0x47000000 a register (set once per thread),
-// so each sample costs exactly one PRMT
-template <uint32_t SEL>
-__device__ __forceinline__ float px_f(uint32_t w, uint32_t magic) {
-  uint32_t r;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(magic), "n"(SEL));
-  return __uint_as_float(r);
-}
-
-
-template <class MP, int R>
-__device__ __forceinline__ float block_sse_u8(const MP& m, const uint2 (&rows)[8], uint32_t magic) {
-  constexpr uint64_t KEEP = keep_mask(R);
-  constexpr bool RESID = popc64(KEEP) > 32;
-  constexpr uint64_t NZ = RESID ? ~KEEP : KEEP;
-  constexpr uint32_t ROWS = row_mask(NZ);
-  if constexpr (NZ == 0) {
-    return 0.0f;
-  } else {
-    float sv[4][8], tv[4][8], p[8][8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float xc[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t w = j < 4 ? rows[i].x : rows[i].y;
-        switch (j & 3) {
-          case 0: xc[i] = px_f<0x7504u>(w, magic); break;
-          case 1: xc[i] = px_f<0x7514u>(w, magic); break;
-          case 2: xc[i] = px_f<0x7524u>(w, magic); break;
-          default: xc[i] = px_f<0x7534u>(w, magic); break;
-        }
-      }
-      float s[4], t[4], col[8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        s[i] = xc[i] + xc[7 - i];
-        t[i] = xc[i] - xc[7 - i];
-        sv[i][j] = s[i] - 2.0f * kSampleBias;
-        tv[i][j] = t[i];
-      }
-      fwd8_st(m, s, t, col);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) p[k][j] = col[k];
-    }
-    float q[8][8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (!((ROWS >> k) & 1u)) continue;
-      float y[8], z[8];
-      fwd8(m, p[k], y);
-#pragma unroll
-      for (int l = 0; l < 8; ++l)
-        z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? (y[l] - m.ybias(k, l)) * m.wy2(k, l) : 0.0f;
-#define ADCT_ROWINV(K)                                                          \
-  if (k == K) {                                                                 \
-    constexpr uint32_t rm = (uint32_t)((NZ >> (8 * K)) & 0xffull);              \
-    if constexpr (rm != 0) inv8<MP, rm>(m, z, q[K]);                            \
-  }
-      ADCT_ROWINV(0) ADCT_ROWINV(1) ADCT_ROWINV(2) ADCT_ROWINV(3)
-      ADCT_ROWINV(4) ADCT_ROWINV(5) ADCT_ROWINV(6) ADCT_ROWINV(7)
-#undef ADCT_ROWINV
-    }
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float col[8], e[4], o[4];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) col[k] = ((ROWS >> k) & 1u) ? q[k][j] : 0.0f;
-      inv8_eo<MP, ROWS>(m, col, e, o);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if constexpr (RESID) {
-          acc[i] = fmaf(e[i], e[i], acc[i]);
-          acc[i] = fmaf(o[i], o[i], acc[i]);
-        } else {
-          const float dp = sv[i][j] - e[i], dm = tv[i][j] - o[i];
-          acc[i] = fmaf(dp, dp, acc[i]);
-          acc[i] = fmaf(dm, dm, acc[i]);
-        }
-      }
-    }
-    return 0.5f * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
-  }
-}
-
-template <class MP, int R>
-__global__ void __launch_bounds__(NT) fused_u8_kernel(const uint8_t* __restrict__ src, KGeom g, DevMat dm,
-                                                      FastDiv dbw, int32_t chunks, double* __restrict__ partial,
-                                                      uint32_t magic /* 0x47000000, kept in a register */) {
-  __shared__ double red[NT / 32];
-  const MP m(dm);
-  const uint8_t* base = src + (int64_t)blockIdx.y * g.image_stride;
-  const uint32_t q0 = blockIdx.x * (NT * BPT_U8) + threadIdx.x;
-  uint2 a[8], b[8], c[8];
-  double acc = 0.0;
-  if (q0 < g.nbi) load_rows(base, g, dbw, q0, a);
-  if (q0 + NT < g.nbi) load_rows(base, g, dbw, q0 + NT, b);
-#pragma unroll 1
-  for (int mb = 0; mb < BPT_U8; mb += 3) {
-    const uint32_t qa = q0 + mb * NT, qb = qa + NT, qc = qb + NT;
-    if (qc < g.nbi) load_rows(base, g, dbw, qc, c);
-    if (qa < g.nbi) acc += (double)block_sse_u8<MP, R>(m, a, magic);
-    if (mb + 3 < BPT_U8 && qc + NT < g.nbi) load_rows(base, g, dbw, qc + NT, a);
-    if (qb < g.nbi) acc += (double)block_sse_u8<MP, R>(m, b, magic);
-    if (mb + 4 < BPT_U8 && qc + 2 * NT < g.nbi) load_rows(base, g, dbw, qc + 2 * NT, b);
-    if (qc < g.nbi) acc += (double)block_sse_u8<MP, R>(m, c, magic);
-  }
-  const double tot = block_sum<NT>(acc, red);
-  if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * chunks + blockIdx.x] = tot;
-}
-
 template <typename SrcT, class MP, int R, int CLIP>
 __global__ void __launch_bounds__(NT) fused_single_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm,
                                                           FastDiv dbw, int32_t chunks,
@@ -232,75 +100,6 @@ __global__ void __launch_bounds__(NT) fused_single_kernel(const SrcT* __restrict
   }
   const double tot = block_sum<NT>(acc, red);
   if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * chunks + blockIdx.x] = tot;
-}
-
-// ---- any list of r: incremental inverse of the dropped coefficients ----------------------
-// Coefficients are added in decreasing zig-zag rank z = 63..1; after adding rank z the
-// register block e = H (W o Y o [rank >= z]) H^T is x - x_hat for r = z.  Each step is a
-// rank-one update e += (w y)_z h_k h_l^T (the inverse applied to one coefficient).
-template <typename SrcT, class MP, int CLIP>
-__global__ void __launch_bounds__(NT) fused_sweep_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm,
-                                                         FastDiv dbw, int32_t chunks, uint64_t rmask, int32_t rmin,
-                                                         double* __restrict__ partial) {
-  __shared__ float zacc[64][NT];
-  __shared__ double red[NT / 32];
-  const MP m(dm);
-#pragma unroll
-  for (int z = 0; z < 64; ++z) zacc[z][threadIdx.x] = 0.0f;
-  const SrcT* base = src + (int64_t)blockIdx.y * g.image_stride;
-  const uint32_t q0 = blockIdx.x * (NT * BPT) + threadIdx.x;
-#pragma unroll 1
-  for (int mb = 0; mb < BPT; ++mb) {
-    const uint32_t q = q0 + mb * NT;
-    if (q >= g.nbi) break;
-    typename Src<SrcT>::Row rows[8];
-    load_rows(base, g, dbw, q, rows);
-    float x[8][8], y[8][8], e[8][8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) Src<SrcT>::to_f(rows[i], x[i]);
-    fwd2d(m, x, y);
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) e[i][j] = 0.0f;
-#pragma unroll
-    for (int zr = 63; zr >= 1; --zr) {
-      if (zr < rmin) break;
-      const int pos = zz_order_at(zr);
-      const int k = pos >> 3, l = pos & 7;
-      const float c = y[k][l] * m.wy(k, l);
-      float a[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = fmac<MP>(m.h(i, k), c, -0.0f);
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) e[i][j] = fmac<MP>(m.h(j, l), a[i], e[i][j]);
-      if ((rmask >> zr) & 1ull) {
-        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float d = (CLIP == ADCT_CLIP_NONE)
-                                ? e[i][j]
-                                : x[i][j] - clipv<CLIP>(x[i][j] - e[i][j], Src<SrcT>::lo, Src<SrcT>::hi);
-            s[j & 3] = fmaf(d, d, s[j & 3]);
-          }
-        zacc[zr - 1][threadIdx.x] += (s[0] + s[1]) + (s[2] + s[3]);
-      }
-    }
-  }
-  __syncthreads();
-  // r = z+1 slots 0..62 (slot 63, r = 64, stays 0: nothing dropped)
-  for (int z = 0; z < 64; ++z) {
-    if (z == 63 || !((rmask >> (z + 1)) & 1ull)) {
-      if (threadIdx.x == 0) partial[((int64_t)blockIdx.y * chunks + blockIdx.x) * 64 + z] = 0.0;
-      continue;
-    }
-    const double tot = block_sum<NT>((double)zacc[z][threadIdx.x], red);
-    if (threadIdx.x == 0) partial[((int64_t)blockIdx.y * chunks + blockIdx.x) * 64 + z] = tot;
-  }
 }
 
 // ---- config 3: forward with S folded into a uniform quantiser ------------------------------
@@ -376,27 +175,6 @@ bool launch_single(int r, dim3 grid, cudaStream_t st, const SrcT* src, const KGe
   }
 }
 
-template <typename SrcT, class MP, int CLIP>
-void launch_sweep(dim3 grid, cudaStream_t st, const SrcT* src, const KGeom& kg, const DevMat& dm, const FastDiv& dbw,
-                  int32_t chunks, uint64_t rmask, int32_t rmin, double* partial) {
-  fused_sweep_kernel<SrcT, MP, CLIP><<<grid, NT, 0, st>>>(src, kg, dm, dbw, chunks, rmask, rmin, partial);
-}
-
-template <class MP>
-bool launch_u8(int r, dim3 grid, cudaStream_t st, const uint8_t* src, const KGeom& kg, const DevMat& dm,
-               const FastDiv& dbw, int32_t chunks, double* partial) {
-  switch (r) {
-#define ADCT_U8_CASE(R)                                                                   \
-  case R:                                                                                 \
-    fused_u8_kernel<MP, R><<<grid, NT, 0, st>>>(src, kg, dm, dbw, chunks, partial, 0x47000000u);       \
-    return true;
-    ADCT_U8_CASE(1) ADCT_U8_CASE(3) ADCT_U8_CASE(6) ADCT_U8_CASE(10) ADCT_U8_CASE(14)
-    ADCT_U8_CASE(15) ADCT_U8_CASE(21) ADCT_U8_CASE(28) ADCT_U8_CASE(36) ADCT_U8_CASE(64)
-#undef ADCT_U8_CASE
-    default:
-      return false;
-  }
-}
 
 template <typename SrcT, class MP>
 adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geom& g, const int32_t* r_list,
@@ -409,11 +187,9 @@ adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geo
   bool single = false;
   if (n_r == 1) {
     if constexpr (std::is_same<SrcT, uint8_t>::value) {
-      if (clip == ADCT_CLIP_NONE && m->is_int) {
-        const int32_t c8 = (int32_t)fused_chunks(g, kFusedBPTU8);
-        single = launch_u8<MP>(r_list[0], dim3((unsigned)c8, (unsigned)g.n_images), st, s, kg, m->dev, dbw, c8,
-                               partial);
-        if (single) chunks = c8;
+      if (clip == ADCT_CLIP_NONE && m->is_int && !g_disable_stream) {
+        adct_status stt = ADCT_OK;
+        if (fused_u8_stream(m, (const uint8_t*)src, g, r_list[0], sse, partial, st, &stt)) return stt;
       }
     }
     dim3 grid((unsigned)chunks, (unsigned)g.n_images);
@@ -432,12 +208,8 @@ adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geo
       if (r_list[i] < rmin) rmin = r_list[i];
       sm.s[i] = r_list[i] - 1;
     }
-    if (clip == ADCT_CLIP_NONE)
-      launch_sweep<SrcT, MP, ADCT_CLIP_NONE>(grid, st, s, kg, m->dev, dbw, chunks, rmask, rmin, partial);
-    else if (clip == ADCT_CLIP)
-      launch_sweep<SrcT, MP, ADCT_CLIP>(grid, st, s, kg, m->dev, dbw, chunks, rmask, rmin, partial);
-    else
-      launch_sweep<SrcT, MP, ADCT_CLIP_ROUND>(grid, st, s, kg, m->dev, dbw, chunks, rmask, rmin, partial);
+    launch_sweep_any(std::is_same<SrcT, uint8_t>::value, MP::kConst, (int)clip, grid, st, s, kg, m->dev, dbw, chunks,
+                     rmask, rmin, partial);
     slots = 64;
   }
   count_launch();

@@ -15,6 +15,15 @@
 namespace adct {
 std::atomic<int64_t> g_launches{0};
 
+int64_t stream_stage_target() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("ADCT_STREAM_STAGE_KB");
+    const long kb = e ? std::atol(e) : 0;
+    return kb > 0 ? (int64_t)kb * 1024 : kStreamStageTargetDefault;
+  }();
+  return v;
+}
+
 namespace {
 
 // the paper's T1 — selects the compile-time network
@@ -269,7 +278,9 @@ size_t adct_workspace_bytes(adct_geom g, int32_t n_r) {
   (void)n_r;  // per-image partials hold all 64 r slots of the sweep kernel
   const int64_t a = fused_chunks(g) * 64;
   const int64_t b = sse_chunks(g);
-  const int64_t per = a > b ? a : b;
+  const int64_t c = stream_partials_per_image(g);
+  int64_t per = a > b ? a : b;
+  if (c > per) per = c;
   return (size_t)(g.n_images > 0 ? g.n_images : 0) * (size_t)per * sizeof(double) + 256;
 }
 

@@ -1,0 +1,625 @@
+// stream.cu — the hot kernel of BASELINE.json config 4: forward -> zonal retention -> inverse
+// -> squared error per image (§6.1) for uint8 planes, with every
+// 8x8 block read from HBM exactly once through a bulk-copy (TMA engine) ring in shared memory.
+//
+// Structure (one persistent CTA per SM, 16 warps):
+//  - warp 0 is the producer: one lane streams "stages" (G consecutive 8-row bands of one
+//    image, contiguous in HBM when rows are unpadded) into a ring of shared-memory slots with
+//    cp.async.bulk, completing on a per-slot "full" mbarrier (transaction bytes);
+//  - warps 1..15 (480 threads) are consumers: each thread owns one 8x8 block of the stage at a
+//    time, reads its 8 rows from shared memory (8 x LDS.64, conflict-free: a warp reads 32
+//    consecutive 8-byte words of one row), runs the fused transform in registers, and the warp
+//    arrives on the slot's "empty" mbarrier when done;
+//  - per stage, each consumer warp reduces its blocks' squared error in a fixed shuffle order
+//    and writes one fp64 partial; finalize_kernel adds an image's partials in index order.
+// Registers, not shared memory, bound the in-flight bytes of the old register-prefetch kernel
+// (160 registers, 12 warps/SM, long-scoreboard stalls; profiles/r01_v0_fused_u8_full.txt);
+// here up to 200 KB per SM are in flight and the compute warps never wait on HBM latency.
+//
+// The block computation (block_sse_u8s) is exact-integer fp32 forward Y = T X T^T (all
+// intermediates are integers < 2^24), weights W = 2/(n_k n_l) folded into the retained
+// coefficients, the inverse x_hat = T^T (W o Y') T of the retained coefficients, and the
+// squared error.  The inverse's last (vertical) butterfly x_hat_i = E_i + O_i,
+// x_hat_{7-i} = E_i - O_i is fused with the error through the forward's first butterfly
+// s_i = x_i + x_{7-i}, t_i = x_i - x_{7-i}:
+//   (x_i - x_hat_i)^2 + (x_{7-i} - x_hat_{7-i})^2 = ((s_i - 2E_i)^2 + (t_i - 2O_i)^2) / 2.
+// For r > 32 the inverse of the dropped coefficients is formed instead (x - x_hat directly,
+// exactly 0 at r = 64; reading A17).  Samples enter fp32 with one PRMT each (pxf).
+#include <cstdlib>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstring>
+#include <mutex>
+
+#include "adct_host.h"
+
+namespace adct {
+
+void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
+                     int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st);
+
+namespace {
+
+__host__ __device__ constexpr int popc64s(uint64_t v) {
+  int c = 0;
+  for (int i = 0; i < 64; ++i) c += (int)((v >> i) & 1u);
+  return c;
+}
+__host__ __device__ constexpr uint32_t row_mask_s(uint64_t nz) {
+  uint32_t r = 0;
+  for (int k = 0; k < 8; ++k)
+    if ((nz >> (8 * k)) & 0xffull) r |= 1u << k;
+  return r;
+}
+
+// ---- mbarrier / bulk-copy primitives (PTX ISA: mbarrier, cp.async.bulk) ----------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+
+// Byte B of w as fp32 M + x with M = 2^15: one PRMT builds the bit pattern 0x4700xx00 from the
+// constant 0x47000000 (held in a register).  PRMT issues on the ALU pipe at half rate, next to
+// the FP32 work; I2F.U8 (byte-select convert) would run on the quarter-rate XU pipe
+// (profiles/r01_probe_pipes.txt) and throttle the kernel.  Every row of T but the first sums
+// to zero, so the bias only enters Y_00 (removed exactly in the weighting) and the sums
+// s_i = x_i + x_{7-i} kept for the error (removed exactly, integers < 2^24).
+template <uint32_t SEL>
+__device__ __forceinline__ float pxf(uint32_t w, uint32_t magic) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(magic), "n"(SEL));
+  return __uint_as_float(r);
+}
+
+// ---- one 8x8 block: SSE of fwd -> retain R -> inv, u8 samples, no clip -------------------------
+template <class MP, int R>
+__device__ __forceinline__ float block_sse_u8s(const MP& m, const uint2 (&rows)[8], uint32_t magic) {
+  constexpr uint64_t KEEP = keep_mask(R);
+  constexpr bool RESID = popc64s(KEEP) > 32;
+  constexpr uint64_t NZ = RESID ? ~KEEP : KEEP;
+  constexpr uint32_t ROWS = row_mask_s(NZ);
+  if constexpr (NZ == 0) {
+    return 0.0f;  // r = 64: nothing dropped, x_hat = x
+  } else {
+    // vertical pass of the forward, P = T X (columns j), keeping s, t for the error
+    float sv[4][8], tv[4][8], p[8][8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float xc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t w = j < 4 ? rows[i].x : rows[i].y;
+        switch (j & 3) {
+          case 0: xc[i] = pxf<0x7504u>(w, magic); break;
+          case 1: xc[i] = pxf<0x7514u>(w, magic); break;
+          case 2: xc[i] = pxf<0x7524u>(w, magic); break;
+          default: xc[i] = pxf<0x7534u>(w, magic); break;
+        }
+      }
+      float s[4], t[4], col[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        s[i] = xc[i] + xc[7 - i];
+        t[i] = xc[i] - xc[7 - i];
+        sv[i][j] = s[i] - 2.0f * kSampleBias;
+        tv[i][j] = t[i];
+      }
+      fwd8_st(m, s, t, col);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[k][j] = col[k];
+    }
+    // horizontal pass Y = P T^T on the rows that hold retained (or dropped) coefficients,
+    // weighting, and the horizontal pass of the inverse Q = (W o Y') T
+    float q[8][8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (!((ROWS >> k) & 1u)) continue;
+      float y[8], z[8];
+      fwd8(m, p[k], y);
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? (y[l] - m.ybias(k, l)) * m.wy2(k, l) : 0.0f;
+#define ADCT_ROWINV_S(K)                                                        \
+  if (k == K) {                                                                 \
+    constexpr uint32_t rm = (uint32_t)((NZ >> (8 * K)) & 0xffull);              \
+    if constexpr (rm != 0) inv8<MP, rm>(m, z, q[K]);                            \
+  }
+      ADCT_ROWINV_S(0) ADCT_ROWINV_S(1) ADCT_ROWINV_S(2) ADCT_ROWINV_S(3)
+      ADCT_ROWINV_S(4) ADCT_ROWINV_S(5) ADCT_ROWINV_S(6) ADCT_ROWINV_S(7)
+#undef ADCT_ROWINV_S
+    }
+    // vertical pass of the inverse up to its last butterfly, fused with the error:
+    // dp_i = s_i - 2E_i, dm_i = t_i - 2O_i (the factor 2 is in the weights)
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float col[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) col[k] = ((ROWS >> k) & 1u) ? q[k][j] : 0.0f;
+      if constexpr (RESID) {
+        float e[4], o[4];
+        inv8_eo<MP, ROWS>(m, col, e, o);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[i] = fmaf(e[i], e[i], acc[i]);
+          acc[i] = fmaf(o[i], o[i], acc[i]);
+        }
+      } else {
+        float e[4];
+        inv8_e<MP, ROWS>(m, col, e);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float dp = sv[i][j] - e[i];
+          const float dm = lsub<MP, 8, ROWS & 0xaau>(tv[i][j], [&](int k) { return m.h(i, k); }, col);
+          acc[i] = fmaf(dp, dp, acc[i]);
+          acc[i] = fmaf(dm, dm, acc[i]);
+        }
+      }
+    }
+    return 0.5f * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+  }
+}
+
+struct StreamArgs {
+  const uint8_t* src;
+  int64_t image_stride, row_stride;  // bytes
+  int32_t width;                     // bytes per row (= W for u8)
+  int32_t bw, bh;                    // blocks per row, bands per image
+  int32_t G, G0, spi, cpi, ns;       // bands per stage / per group, stages and chunks per image, ring slots
+  int64_t n_chunks;
+  int32_t stage_bytes;
+  int32_t contiguous;                // rows of an image unpadded: one copy per stage
+  FastDiv dbw;                       // division by bw
+};
+
+// producer wait on a slot's "empty" barrier: the ring has slack, so sleep between probes
+// instead of spinning on the issue slots the consumer warps need
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 2000;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(500);
+  }
+}
+
+// Work unit: a chunk = up to kStreamChunkStages consecutive stages of one image.  CTA b takes
+// chunks b, b + gridDim.x, ...; the per-(chunk, consumer warp) fp64 partial is grid-independent.
+template <class MP, int R>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    fused_u8_stream_kernel(StreamArgs a, DevMat dm, double* __restrict__ partial, uint32_t magic) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (int64_t)a.ns * a.stage_bytes);
+  uint64_t* empty = full + a.ns;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < a.ns; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kStreamConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---- producer --------------------------------------------------------------------------
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t phase = 0;  // parity of the slot's current round
+      uint32_t k = 0;
+      for (int64_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
+        const int64_t img = cg / a.cpi;
+        const int32_t st0 = (int32_t)(cg - img * a.cpi) * kStreamChunkStages;
+        const int32_t st1 = min(a.spi, st0 + kStreamChunkStages);
+        const uint8_t* isrc = a.src + img * a.image_stride;
+        for (int32_t stg = st0; stg < st1; ++stg, ++k) {
+          if (k >= (uint32_t)a.ns) mbar_wait_sleep(&empty[slot], phase ^ 1u);
+          const int32_t b0 = stg * a.G;
+          const int32_t nb = min(a.G, a.bh - b0);
+          const uint32_t bytes = (uint32_t)nb * 8u * (uint32_t)a.width;
+          uint8_t* dst = ring + (int64_t)slot * a.stage_bytes;
+          const uint8_t* src = isrc + (int64_t)b0 * 8 * a.row_stride;
+          mbar_arrive_expect_tx(&full[slot], bytes);
+          if (a.contiguous) {
+            bulk_g2s(dst, src, bytes, &full[slot]);
+          } else {
+            for (int r = 0; r < nb * 8; ++r)
+              bulk_g2s(dst + (int64_t)r * a.width, src + (int64_t)r * a.row_stride, (uint32_t)a.width, &full[slot]);
+          }
+          if (++slot == a.ns) { slot = 0; phase ^= 1u; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ------------------------------------------------------------------------------
+  const MP m(dm);
+  const int ct = threadIdx.x - 32;          // 0 .. 479
+  const int cw = warp - 1;                  // consumer warp 0 .. 14
+  const uint32_t ring_u32 = smem_u32(ring);
+  const uint32_t W = (uint32_t)a.width;
+  // fixed mapping (bw divides the consumer count): this thread's block in every group of G0 bands
+  const uint32_t gband = a.G0 ? (uint32_t)ct / (uint32_t)a.bw : 0u;
+  const uint32_t toff = a.G0 ? gband * 8u * W + ((uint32_t)ct - gband * (uint32_t)a.bw) * 8u : 0u;
+  const uint32_t gstep = (uint32_t)a.G0 * 8u * W;
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int64_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
+    const int64_t img = cg / a.cpi;
+    const int32_t st0 = (int32_t)(cg - img * a.cpi) * kStreamChunkStages;
+    const int32_t st1 = min(a.spi, st0 + kStreamChunkStages);
+    float acc = 0.0f;
+    for (int32_t stg = st0; stg < st1; ++stg) {
+      const int32_t nb = min(a.G, a.bh - stg * a.G);
+      mbar_wait(&full[slot], phase);
+      const uint32_t base = ring_u32 + (uint32_t)slot * (uint32_t)a.stage_bytes;
+      if (a.G0) {
+        uint32_t p = base + toff;
+        for (int32_t g0 = 0; g0 < nb; g0 += a.G0, p += gstep) {
+          if ((int32_t)gband < nb - g0) {
+            uint2 rows[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)i * W);
+            acc += block_sse_u8s<MP, R>(m, rows, magic);
+          }
+        }
+      } else {
+        const int32_t nblk = nb * a.bw;
+        for (int32_t q = ct; q < nblk; q += kStreamConsumers) {
+          const uint32_t band = fdiv((uint32_t)q, a.dbw);
+          const uint32_t bx = (uint32_t)q - band * (uint32_t)a.bw;
+          const uint32_t p = base + band * 8u * W + bx * 8u;
+          uint2 rows[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)i * W);
+          acc += block_sse_u8s<MP, R>(m, rows, magic);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == a.ns) { slot = 0; phase ^= 1u; }
+    }
+    // per-(chunk, warp) partial, fixed shuffle order
+    double v = (double)acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) partial[cg * kStreamConsumerWarps + cw] = v;
+  }
+}
+
+// ---- warp-tile kernel ----------------------------------------------------------------------------
+struct WtArgs {
+  int32_t tpb, tpi, cpi;  // tiles per band pair / per image, chunks per image
+  uint32_t n_chunks;
+  FastDiv dcpi, dtpb;
+};
+
+// The warp's walk over its tiles: chunks cg = blockIdx.x, +gridDim.x, ...; inside chunk cg the
+// warp takes tiles w, w + 16, ... (< n).  Positions advance incrementally (no divisions per tile).
+struct WtIt {
+  uint32_t cg;
+  int32_t j, n;
+  uint32_t img;
+  int32_t pair, slice;  // tile row (16 image rows) and column (256 bytes)
+};
+
+__device__ __forceinline__ void wt_enter(const WtArgs& a, int w, WtIt& it) {
+  while (it.cg < a.n_chunks) {  // first chunk at or after it.cg in which this warp has a tile
+    it.img = fdiv(it.cg, a.dcpi);
+    const int32_t c = (int32_t)(it.cg - it.img * (uint32_t)a.cpi);
+    it.n = min(kWtChunkTiles, a.tpi - c * kWtChunkTiles);
+    if (w < it.n) {
+      const uint32_t tt = (uint32_t)(c * kWtChunkTiles + w);
+      it.pair = (int32_t)fdiv(tt, a.dtpb);
+      it.slice = (int32_t)tt - it.pair * a.tpb;
+      it.j = 0;
+      return;
+    }
+    it.cg += gridDim.x;
+  }
+}
+
+// advance to the next tile; returns true when the chunk changed
+__device__ __forceinline__ bool wt_next(const WtArgs& a, int w, WtIt& it) {
+  ++it.j;
+  if (w + kWtWarps * it.j < it.n) {
+    it.slice += kWtWarps;
+    while (it.slice >= a.tpb) {
+      it.slice -= a.tpb;
+      ++it.pair;
+    }
+    return false;
+  }
+  it.cg += gridDim.x;
+  wt_enter(a, w, it);
+  return true;
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int32_t x, int32_t y, int32_t z,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
+
+template <class MP, int R>
+__global__ void __launch_bounds__(kWtThreads, 1)
+    fused_u8_wtile_kernel(const __grid_constant__ CUtensorMap tmap, WtArgs a, DevMat dm, double* __restrict__ partial,
+                          uint32_t magic) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wring = smem + (size_t)w * kWtSlots * kWtTileBytes;
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + (size_t)kWtWarps * kWtSlots * kWtTileBytes) + w * kWtSlots;
+  if (lane == 0) {
+    for (int i = 0; i < kWtSlots; ++i) mbar_init(&wfull[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const MP m(dm);
+  const uint32_t ring0 = smem_u32(wring), full0 = smem_u32(wfull);
+
+  // prefetch walk: the same tile sequence the warp consumes, kWtSlots tiles ahead (lane 0)
+  WtIt pf;
+  pf.cg = blockIdx.x;
+  wt_enter(a, w, pf);
+  auto issue = [&](int slot) {
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + slot * 8),
+                   "r"((uint32_t)kWtTileBytes)
+                   : "memory");
+      tma_load_3d(ring0 + slot * kWtTileBytes, &tmap, pf.slice * kWtSlice, pf.pair * kWtRows, (int32_t)pf.img,
+                  full0 + slot * 8);
+    }
+    wt_next(a, w, pf);
+  };
+#pragma unroll 1
+  for (int s = 0; s < kWtSlots; ++s)
+    if (pf.cg < a.n_chunks) issue(s);
+
+  const uint32_t lane_u32 = ring0 + (uint32_t)lane * 8u;
+  int slot = 0;
+  uint32_t phase = 0;
+  WtIt it;
+  it.cg = blockIdx.x;
+  wt_enter(a, w, it);
+  float acc = 0.0f;
+  // chunks in which this warp has no tile keep a zero partial
+  if (lane == 0)
+    for (uint32_t cz = blockIdx.x; cz < min(it.cg, a.n_chunks); cz += gridDim.x) partial[(int64_t)cz * kWtWarps + w] = 0.0;
+  while (it.cg < a.n_chunks) {
+    mbar_wait(&wfull[slot], phase);
+    const uint32_t p = lane_u32 + (uint32_t)slot * kWtTileBytes;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {  // the lane's block in band 0 and band 1 of the tile
+      uint2 rows[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)(b * 8 + i) * kWtSlice);
+      acc += block_sse_u8s<MP, R>(m, rows, magic);
+    }
+    __syncwarp();
+    // the slot was read through the generic proxy; order that before the async-proxy refill
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (pf.cg < a.n_chunks) issue(slot);
+    if (++slot == kWtSlots) { slot = 0; phase ^= 1u; }
+    const uint32_t cg = it.cg;
+    if (wt_next(a, w, it)) {  // chunk done: per-(chunk, warp) partial in a fixed shuffle order
+      double v = (double)acc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        partial[(int64_t)cg * kWtWarps + w] = v;
+        for (uint32_t cz = cg + gridDim.x; cz < min(it.cg, a.n_chunks); cz += gridDim.x)
+          partial[(int64_t)cz * kWtWarps + w] = 0.0;
+      }
+      acc = 0.0f;
+    }
+  }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+bool make_u8_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.width, (cuuint64_t)g.height, (cuuint64_t)g.n_images};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.row_stride,
+                                 (cuuint64_t)(g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride)};
+  const cuuint32_t box[3] = {(cuuint32_t)kWtSlice, (cuuint32_t)kWtRows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(src), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int g_sms_s = 0;
+int sms_s() {
+  if (!g_sms_s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms_s, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms_s <= 0) g_sms_s = 148;
+  }
+  return g_sms_s;
+}
+
+template <class MP, int R>
+bool launch_stream_r(const StreamArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
+  const size_t smem = (size_t)a.ns * a.stage_bytes + 2 * sizeof(uint64_t) * a.ns;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(fused_u8_stream_kernel<MP, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(kStreamSmemBudget + 1024));
+  });
+  if (attr_err != cudaSuccess) return false;
+  const int64_t grid = a.n_chunks < sms_s() ? a.n_chunks : sms_s();
+  fused_u8_stream_kernel<MP, R><<<(unsigned)grid, kStreamThreads, smem, st>>>(a, dm, partial, 0x47000000u);
+  return true;
+}
+
+template <class MP, int R>
+bool launch_wtile_r(const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(fused_u8_wtile_kernel<MP, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kWtSmem);
+  });
+  if (attr_err != cudaSuccess) return false;
+  const int64_t grid = (int64_t)a.n_chunks < sms_s() ? (int64_t)a.n_chunks : sms_s();
+  fused_u8_wtile_kernel<MP, R><<<(unsigned)grid, kWtThreads, kWtSmem, st>>>(map, a, dm, partial, 0x47000000u);
+  return true;
+}
+
+template <class MP>
+bool launch_wtile(int r, const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial,
+                  cudaStream_t st) {
+  switch (r) {
+#define ADCT_WT_CASE(R) \
+  case R:               \
+    return launch_wtile_r<MP, R>(map, a, dm, partial, st);
+    ADCT_WT_CASE(1) ADCT_WT_CASE(3) ADCT_WT_CASE(6) ADCT_WT_CASE(10) ADCT_WT_CASE(14)
+    ADCT_WT_CASE(15) ADCT_WT_CASE(21) ADCT_WT_CASE(28) ADCT_WT_CASE(36)
+#undef ADCT_WT_CASE
+    default:
+      return false;
+  }
+}
+
+const int g_stream_mode = [] {  // ADCT_STREAM_MODE=stage selects the stage-ring kernel
+  const char* e = std::getenv("ADCT_STREAM_MODE");
+  return (e && e[0] == 's') ? 1 : 0;
+}();
+
+template <class MP>
+bool launch_stream(int r, const StreamArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
+  switch (r) {
+#define ADCT_STREAM_CASE(R) \
+  case R:                   \
+    return launch_stream_r<MP, R>(a, dm, partial, st);
+    ADCT_STREAM_CASE(1) ADCT_STREAM_CASE(3) ADCT_STREAM_CASE(6) ADCT_STREAM_CASE(10) ADCT_STREAM_CASE(14)
+    ADCT_STREAM_CASE(15) ADCT_STREAM_CASE(21) ADCT_STREAM_CASE(28) ADCT_STREAM_CASE(36)
+#undef ADCT_STREAM_CASE
+    default:
+      return false;
+  }
+}
+
+}  // namespace
+
+// The streaming path for (u8 source, integer matrix, no clip, one r); returns false when the
+// geometry or r is not covered (the caller then uses the register-prefetch kernels).
+// On success the per-image SSE is in sse[n_images] (finalize launched on st).
+bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
+                     double* partial, cudaStream_t st, adct_status* status) {
+  if (g_stream_mode == 0) {
+    const WtPlan p = wt_plan(g);
+    if (!p.ok || g.n_images == 0 || !aligned(src, 16)) return false;
+    CUtensorMap map;
+    if (!make_u8_tmap(&map, src, g)) return false;
+    WtArgs a;
+    a.tpb = p.tpb;
+    a.tpi = p.tpi;
+    a.cpi = p.cpi;
+    a.n_chunks = (uint32_t)p.n_chunks;
+    a.dcpi = make_fastdiv((uint32_t)p.cpi);
+    a.dtpb = make_fastdiv((uint32_t)p.tpb);
+    const bool ok = m->specialized ? launch_wtile<T1Mat>(r, map, a, m->dev, partial, st)
+                                   : launch_wtile<RtMat>(r, map, a, m->dev, partial, st);
+    if (!ok) return false;
+    count_launch();
+    if ((*status = launch_status()) != ADCT_OK) return true;
+    SlotMap sm{};
+    sm.s[0] = 0;
+    launch_finalize(partial, p.cpi * kWtWarps, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0, sse,
+                    nullptr, st);
+    *status = launch_status();
+    return true;
+  }
+  const StreamPlan p = stream_plan(g);
+  if (!p.ok || g.n_images == 0) return false;
+  if (!aligned(src, 16)) return false;
+  StreamArgs a;
+  a.src = src;
+  a.image_stride = g.image_stride;
+  a.row_stride = g.row_stride;
+  a.width = g.width;
+  a.bw = g.width / 8;
+  a.bh = g.height / 8;
+  a.G = p.G;
+  a.G0 = p.G0;
+  a.spi = p.spi;
+  a.cpi = p.cpi;
+  a.ns = p.stages_in_ring;
+  a.n_chunks = p.n_chunks;
+  a.stage_bytes = (int32_t)p.stage_bytes;
+  a.contiguous = (g.row_stride == g.width) ? 1 : 0;
+  a.dbw = make_fastdiv((uint32_t)a.bw);
+  const bool ok = m->specialized ? launch_stream<T1Mat>(r, a, m->dev, partial, st)
+                                 : launch_stream<RtMat>(r, a, m->dev, partial, st);
+  if (!ok) return false;
+  count_launch();
+  if ((*status = launch_status()) != ADCT_OK) return true;
+  SlotMap sm{};
+  sm.s[0] = 0;
+  launch_finalize(partial, p.cpi * kStreamConsumerWarps, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0,
+                  sse, nullptr, st);
+  *status = launch_status();
+  return true;
+}
+
+}  // namespace adct

@@ -3,6 +3,7 @@
 // Not part of the product; decides FP32-pair vs packed-int16 arithmetic.
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o probes/pipes probes/pipes.cu
+#include <cstdlib>
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -53,6 +54,22 @@ __global__ void __launch_bounds__(1024) pipe_kernel(const uint32_t* in, uint32_t
       if (OP == 16) f2[i] = __fmul2_rn(f2[i], fa);                                              // FMUL2
       if (OP == 17) asm volatile("fma.rn.f32 %0, %1, %1, %0;" : "+r"(r[i]) : "r"(a0));           // FFMA acc (2 distinct regs)
       if (OP == 18) asm volatile("sub.f32 %0, %1, %0;" : "+r"(r[i]) : "r"(a0));                  // FADD variant
+      if (OP == 19) asm volatile("{.reg .b32 t; shr.b32 t, %0, 8; cvt.rn.f32.u8 %0, t;}" : "+r"(r[i]));  // I2F.U8 .B1
+      if (OP == 20) {  // I2F.U8 .B1 + FFMA interleaved
+        asm volatile("{.reg .b32 t; shr.b32 t, %0, 8; cvt.rn.f32.u8 %0, t;}" : "+r"(r[i]));
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+r"(r[(i + 4) & 7]) : "r"(a0), "r"(a1));
+      }
+      if (OP == 21) asm volatile("{.reg .b32 t; shr.b32 t, %0, 16; cvt.rn.f32.s16 %0, t;}" : "+r"(r[i]));  // I2F.S16 .H1
+      if (OP == 22) {  // PRMT + FFMA interleaved
+        asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(r[i]) : "r"(a0));
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+r"(r[(i + 4) & 7]) : "r"(a0), "r"(a1));
+      }
+      if (OP == 23) {  // FFMA + FADD + I2F.U8 (2:1 FMA-pipe : conversion)
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+r"(r[(i + 4) & 7]) : "r"(a0), "r"(a1));
+        asm volatile("add.f32 %0, %0, %1;" : "+r"(r[(i + 2) & 7]) : "r"(a0));
+        asm volatile("{.reg .b32 t; shr.b32 t, %0, 8; cvt.rn.f32.u8 %0, t;}" : "+r"(r[i]));
+      }
+      if (OP == 24) asm volatile("cvt.rn.f32.u8 %0, %0;" : "+r"(r[i]));  // I2F.U8 .B0
     }
   }
   long long t1 = clock64();
@@ -97,7 +114,8 @@ __global__ void read_blocks_u8(const uint8_t* __restrict__ img, int W, int H, in
 
 static const char* names[] = {"FFMA(3reg)", "FFMA(imm)", "FADD", "FFMA2", "FADD2", "IADD3", "LOP3", "PRMT", "LEA",
                               "IMAD", "I2FP.U32", "HFMA2", "FFMA2+IADD3", "FFMA+IADD3", "I2F.S32", "FMUL", "FMUL2",
-                              "FFMA(acc a*a+d)", "FADD(sub)"};
+                              "FFMA(acc a*a+d)", "FADD(sub)", "I2F.U8.B1", "I2F.U8.B1+FFMA", "I2F.S16.H1",
+                              "PRMT+FFMA", "FFMA+FADD+I2F.U8", "I2F.U8.B0"};
 
 template <int OP>
 int run_one(const uint32_t* din, uint32_t* dout, long long* dcyc, int nsm) {
@@ -111,7 +129,7 @@ int run_one(const uint32_t* din, uint32_t* dout, long long* dcyc, int nsm) {
   double mean = 0;
   for (int i = 0; i < nsm; ++i) mean += (double)h[i];
   mean /= nsm;
-  int per = (OP == 12 || OP == 13) ? 16 : 8;
+  int per = (OP == 12 || OP == 13 || OP == 20 || OP == 22) ? 16 : (OP == 23 ? 24 : 8);
   double warp_inst = 32.0 * ITERS * per;  // warp-instructions per SM (32 warps)
   printf("%-18s %7.3f warp-inst/clk/SM  (%5.3f per SMSP)\n", names[OP], warp_inst / mean, warp_inst / mean / 4);
   return 0;
@@ -138,7 +156,10 @@ int main() {
   run_one<9>(din, dout, dcyc, nsm);  run_one<10>(din, dout, dcyc, nsm); run_one<11>(din, dout, dcyc, nsm);
   run_one<12>(din, dout, dcyc, nsm); run_one<13>(din, dout, dcyc, nsm); run_one<14>(din, dout, dcyc, nsm);
   run_one<15>(din, dout, dcyc, nsm); run_one<16>(din, dout, dcyc, nsm); run_one<17>(din, dout, dcyc, nsm);
-  run_one<18>(din, dout, dcyc, nsm);
+  run_one<18>(din, dout, dcyc, nsm); run_one<19>(din, dout, dcyc, nsm); run_one<20>(din, dout, dcyc, nsm);
+  run_one<21>(din, dout, dcyc, nsm); run_one<22>(din, dout, dcyc, nsm); run_one<23>(din, dout, dcyc, nsm);
+  run_one<24>(din, dout, dcyc, nsm);
+  if (getenv("PIPES_ONLY")) return 0;
 
   // streaming read bandwidth
   size_t bytes = (size_t)8 << 30;
