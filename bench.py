@@ -290,7 +290,7 @@ def main():
                        "hbm_gbs_step": world * blocks_step_rank * 64 / (ms_step * 1e-3) / 1e9 / world},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "fused_u8_kernel<T1Mat,10> (luma plane, 66,355,200 blocks x 64 B)",
+                         "kernel": "fused_u8_wtile_kernel<T1Mat,10> + finalize_kernel (luma plane, 66,355,200 blocks x 64 B)",
                          "kernel_ms": luma_ms},
             "clocks": clk.summary(),
             "gpu_launches": launches,
