@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libadct.so")
+# ADCT_LIB may name another in-tree build of the same library (kernel A/B runs in tools/gpu)
+LIB_PATH = os.environ.get("ADCT_LIB") or os.path.join(_HERE, "libadct.so")
 
 U8, I16, I32, F32 = 0, 1, 2, 3
 CLIP_NONE, CLIP, CLIP_ROUND = 0, 1, 2

@@ -139,16 +139,17 @@ inline StreamPlan stream_plan(const adct_geom& g, int esz = 1) {
 constexpr int kWtWarps = 16;
 constexpr int kWtThreads = 32 * kWtWarps;
 constexpr int kWtSlots = 3;
-constexpr int kWtSlice = 256;                       // bytes of a row slice = 32 blocks
-constexpr int kWtRows = 16;                         // image rows per tile (2 bands)
-constexpr int kWtTileBytes = kWtRows * kWtSlice;
+constexpr int kWtTileBytes = 4096;                  // 64 blocks: 2 per lane
 constexpr int kWtChunkTiles = kWtWarps * 8;         // 8 tiles per warp per chunk
 constexpr size_t kWtSmem = (size_t)kWtWarps * kWtSlots * kWtTileBytes + (size_t)kWtWarps * kWtSlots * 8 + 128;
 
+// tile shape: tw bytes wide (256 = 32 blocks per band, or 128 = 16 blocks) x 4096/tw rows
+// (2 or 4 bands); the shape that wastes the fewest zero-filled blocks is chosen per geometry
 struct WtPlan {
-  int32_t tpb;      // tiles per band pair (ceil(W / 256))
-  int32_t tpi;      // tiles per image
-  int32_t cpi;      // chunks per image
+  int32_t tw, rows;  // tile width (bytes) and height (rows)
+  int32_t tpb;       // tiles per tile row (ceil(W / tw))
+  int32_t tpi;       // tiles per image
+  int32_t cpi;       // chunks per image
   int64_t n_chunks;
   bool ok;
 };
@@ -156,8 +157,18 @@ inline WtPlan wt_plan(const adct_geom& g) {
   WtPlan p{};
   const int64_t W = g.width, H = g.height;
   if (W <= 0 || H <= 0) return p;
-  p.tpb = (int32_t)((W + kWtSlice - 1) / kWtSlice);
-  p.tpi = (int32_t)(((H + kWtRows - 1) / kWtRows) * p.tpb);
+  int64_t best = -1;
+  for (int tw : {256, 128}) {
+    const int64_t rows = kWtTileBytes / tw;
+    const int64_t tiles = ((W + tw - 1) / tw) * ((H + rows - 1) / rows);
+    if (best < 0 || tiles < best) {  // equal tile counts -> equal waste; keep the wider tile
+      best = tiles;
+      p.tw = tw;
+      p.rows = (int32_t)rows;
+    }
+  }
+  p.tpb = (int32_t)((W + p.tw - 1) / p.tw);
+  p.tpi = (int32_t)(((H + p.rows - 1) / p.rows) * p.tpb);
   p.cpi = (p.tpi + kWtChunkTiles - 1) / kWtChunkTiles;
   p.n_chunks = g.n_images * (int64_t)p.cpi;
   // tensor-map constraints: 16-byte aligned strides (< 2^40), dimensions < 2^32
@@ -168,9 +179,14 @@ inline WtPlan wt_plan(const adct_geom& g) {
 
 inline int64_t stream_partials_per_image(const adct_geom& g) {
   const StreamPlan p = stream_plan(g);
-  const WtPlan w = wt_plan(g);
-  const int64_t a = (int64_t)p.cpi * kStreamConsumerWarps, b = (int64_t)w.cpi * kWtWarps;
-  return a > b ? a : b;
+  int64_t best = (int64_t)p.cpi * kStreamConsumerWarps;
+  for (int tw : {256, 128}) {  // either warp-tile shape may be used (runtime matrices: 256 only)
+    const int64_t rows = kWtTileBytes / tw;
+    const int64_t tpi = ((g.width + tw - 1) / tw) * ((g.height + rows - 1) / rows);
+    const int64_t c = (tpi + kWtChunkTiles - 1) / kWtChunkTiles * kWtWarps;
+    if (c > best) best = c;
+  }
+  return best;
 }
 
 }  // namespace adct

@@ -101,6 +101,21 @@ __device__ __forceinline__ float pxf(uint32_t w, uint32_t magic) {
   return __uint_as_float(r);
 }
 
+// byte B of w as fp32 through I2F.U8 with a byte selector (no bias; quarter-rate XU pipe, used
+// for a few columns only so that the XU pipe works next to the FMA and ALU pipes)
+template <int B>
+__device__ __forceinline__ float ubyte(uint32_t w) {
+  float f;
+  if constexpr (B == 0) asm("cvt.rn.f32.u8 %0, %1;" : "=f"(f) : "r"(w));
+  else asm("{.reg .b32 t; shr.b32 t, %1, %2; cvt.rn.f32.u8 %0, t;}" : "=f"(f) : "r"(w), "n"(8 * B));
+  return f;
+}
+
+#ifndef ADCT_XU_COLS
+#define ADCT_XU_COLS 3
+#endif
+constexpr int kXuCols = ADCT_XU_COLS;  // columns of each block converted on the XU pipe
+
 // ---- one 8x8 block: SSE of fwd -> retain R -> inv, u8 samples, no clip -------------------------
 template <class MP, int R>
 __device__ __forceinline__ float block_sse_u8s(const MP& m, const uint2 (&rows)[8], uint32_t magic) {
@@ -119,22 +134,34 @@ __device__ __forceinline__ float block_sse_u8s(const MP& m, const uint2 (&rows)[
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const uint32_t w = j < 4 ? rows[i].x : rows[i].y;
-        switch (j & 3) {
-          case 0: xc[i] = pxf<0x7504u>(w, magic); break;
-          case 1: xc[i] = pxf<0x7514u>(w, magic); break;
-          case 2: xc[i] = pxf<0x7524u>(w, magic); break;
-          default: xc[i] = pxf<0x7534u>(w, magic); break;
+        if (j < kXuCols) {
+          switch (j & 3) {
+            case 0: xc[i] = ubyte<0>(w); break;
+            case 1: xc[i] = ubyte<1>(w); break;
+            case 2: xc[i] = ubyte<2>(w); break;
+            default: xc[i] = ubyte<3>(w); break;
+          }
+        } else {
+          switch (j & 3) {
+            case 0: xc[i] = pxf<0x7504u>(w, magic); break;
+            case 1: xc[i] = pxf<0x7514u>(w, magic); break;
+            case 2: xc[i] = pxf<0x7524u>(w, magic); break;
+            default: xc[i] = pxf<0x7534u>(w, magic); break;
+          }
         }
       }
-      float s[4], t[4], col[8];
+      // s carries the bias 2M for PRMT-converted columns: removed exactly (integers < 2^24),
+      // and the forward runs on the unbiased sums, so no coefficient carries a bias
+      float t[4], col[8];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        s[i] = xc[i] + xc[7 - i];
+        const float sb = xc[i] + xc[7 - i];
+        sv[i][j] = (j < kXuCols) ? sb : sb - 2.0f * kSampleBias;
         t[i] = xc[i] - xc[7 - i];
-        sv[i][j] = s[i] - 2.0f * kSampleBias;
         tv[i][j] = t[i];
       }
-      fwd8_st(m, s, t, col);
+      float su[4] = {sv[0][j], sv[1][j], sv[2][j], sv[3][j]};
+      fwd8_st(m, su, t, col);
 #pragma unroll
       for (int k = 0; k < 8; ++k) p[k][j] = col[k];
     }
@@ -148,7 +175,7 @@ __device__ __forceinline__ float block_sse_u8s(const MP& m, const uint2 (&rows)[
       fwd8(m, p[k], y);
 #pragma unroll
       for (int l = 0; l < 8; ++l)
-        z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? (y[l] - m.ybias(k, l)) * m.wy2(k, l) : 0.0f;
+        z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? y[l] * m.wy2(k, l) : 0.0f;
 #define ADCT_ROWINV_S(K)                                                        \
   if (k == K) {                                                                 \
     constexpr uint32_t rm = (uint32_t)((NZ >> (8 * K)) & 0xffull);              \
@@ -384,10 +411,17 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-template <class MP, int R>
+#ifndef ADCT_WT_UNROLL
+#define ADCT_WT_UNROLL 2
+#endif
+constexpr int kWtUnroll = ADCT_WT_UNROLL;  // unrolling of the 2-block loop (code size vs ILP)
+
+template <class MP, int R, int TW>
 __global__ void __launch_bounds__(kWtThreads, 1)
     fused_u8_wtile_kernel(const __grid_constant__ CUtensorMap tmap, WtArgs a, DevMat dm, double* __restrict__ partial,
                           uint32_t magic) {
+  constexpr int RT = kWtTileBytes / TW;  // rows per tile
+  constexpr int BPR = TW / 8;            // blocks per band in a tile = lanes per band group
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -410,7 +444,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + slot * 8),
                    "r"((uint32_t)kWtTileBytes)
                    : "memory");
-      tma_load_3d(ring0 + slot * kWtTileBytes, &tmap, pf.slice * kWtSlice, pf.pair * kWtRows, (int32_t)pf.img,
+      tma_load_3d(ring0 + slot * kWtTileBytes, &tmap, pf.slice * TW, pf.pair * RT, (int32_t)pf.img,
                   full0 + slot * 8);
     }
     wt_next(a, w, pf);
@@ -419,7 +453,8 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   for (int s = 0; s < kWtSlots; ++s)
     if (pf.cg < a.n_chunks) issue(s);
 
-  const uint32_t lane_u32 = ring0 + (uint32_t)lane * 8u;
+  // lane -> block column (lane % BPR) and its two bands 2*(lane / BPR), 2*(lane / BPR) + 1
+  const uint32_t lane_u32 = ring0 + (uint32_t)(lane % BPR) * 8u + (uint32_t)(lane / BPR) * 16u * TW;
   int slot = 0;
   uint32_t phase = 0;
   WtIt it;
@@ -432,11 +467,11 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   while (it.cg < a.n_chunks) {
     mbar_wait(&wfull[slot], phase);
     const uint32_t p = lane_u32 + (uint32_t)slot * kWtTileBytes;
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {  // the lane's block in band 0 and band 1 of the tile
+#pragma unroll kWtUnroll
+    for (int b = 0; b < 2; ++b) {  // the lane's two blocks (consecutive bands of the tile)
       uint2 rows[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)(b * 8 + i) * kWtSlice);
+      for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)(b * 8 + i) * TW);
       acc += block_sse_u8s<MP, R>(m, rows, magic);
     }
     __syncwarp();
@@ -472,13 +507,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   return fn;
 }
 
-bool make_u8_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g) {
+bool make_u8_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int tw, int rows) {
   auto enc = tmap_encoder();
   if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)g.width, (cuuint64_t)g.height, (cuuint64_t)g.n_images};
   const cuuint64_t strides[2] = {(cuuint64_t)g.row_stride,
                                  (cuuint64_t)(g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride)};
-  const cuuint32_t box[3] = {(cuuint32_t)kWtSlice, (cuuint32_t)kWtRows, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)tw, (cuuint32_t)rows, 1};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(src), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -511,27 +546,37 @@ bool launch_stream_r(const StreamArgs& a, const DevMat& dm, double* partial, cud
   return true;
 }
 
-template <class MP, int R>
-bool launch_wtile_r(const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
+template <class MP, int R, int TW>
+bool launch_wtile_rt(const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(fused_u8_wtile_kernel<MP, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(fused_u8_wtile_kernel<MP, R, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kWtSmem);
   });
   if (attr_err != cudaSuccess) return false;
   const int64_t grid = (int64_t)a.n_chunks < sms_s() ? (int64_t)a.n_chunks : sms_s();
-  fused_u8_wtile_kernel<MP, R><<<(unsigned)grid, kWtThreads, kWtSmem, st>>>(map, a, dm, partial, 0x47000000u);
+  fused_u8_wtile_kernel<MP, R, TW><<<(unsigned)grid, kWtThreads, kWtSmem, st>>>(map, a, dm, partial, 0x47000000u);
   return true;
 }
 
+// the 128-byte tile shape is compiled for the paper's T1 only; other matrices use 256-byte tiles
+template <class MP, int R>
+bool launch_wtile_r(int tw, const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial,
+                    cudaStream_t st) {
+  if constexpr (MP::kConst) {
+    if (tw == 128) return launch_wtile_rt<MP, R, 128>(map, a, dm, partial, st);
+  }
+  return tw == 256 && launch_wtile_rt<MP, R, 256>(map, a, dm, partial, st);
+}
+
 template <class MP>
-bool launch_wtile(int r, const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial,
+bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial,
                   cudaStream_t st) {
   switch (r) {
 #define ADCT_WT_CASE(R) \
   case R:               \
-    return launch_wtile_r<MP, R>(map, a, dm, partial, st);
+    return launch_wtile_r<MP, R>(tw, map, a, dm, partial, st);
     ADCT_WT_CASE(1) ADCT_WT_CASE(3) ADCT_WT_CASE(6) ADCT_WT_CASE(10) ADCT_WT_CASE(14)
     ADCT_WT_CASE(15) ADCT_WT_CASE(21) ADCT_WT_CASE(28) ADCT_WT_CASE(36)
 #undef ADCT_WT_CASE
@@ -567,10 +612,18 @@ bool launch_stream(int r, const StreamArgs& a, const DevMat& dm, double* partial
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
                      double* partial, cudaStream_t st, adct_status* status) {
   if (g_stream_mode == 0) {
-    const WtPlan p = wt_plan(g);
+    WtPlan p = wt_plan(g);
     if (!p.ok || g.n_images == 0 || !aligned(src, 16)) return false;
+    if (!m->specialized && p.tw != 256) {  // runtime matrices: 256-byte tiles only
+      p.tw = 256;
+      p.rows = kWtTileBytes / 256;
+      p.tpb = (g.width + 255) / 256;
+      p.tpi = ((g.height + p.rows - 1) / p.rows) * p.tpb;
+      p.cpi = (p.tpi + kWtChunkTiles - 1) / kWtChunkTiles;
+      p.n_chunks = g.n_images * (int64_t)p.cpi;
+    }
     CUtensorMap map;
-    if (!make_u8_tmap(&map, src, g)) return false;
+    if (!make_u8_tmap(&map, src, g, p.tw, p.rows)) return false;
     WtArgs a;
     a.tpb = p.tpb;
     a.tpi = p.tpi;
@@ -578,8 +631,8 @@ bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& 
     a.n_chunks = (uint32_t)p.n_chunks;
     a.dcpi = make_fastdiv((uint32_t)p.cpi);
     a.dtpb = make_fastdiv((uint32_t)p.tpb);
-    const bool ok = m->specialized ? launch_wtile<T1Mat>(r, map, a, m->dev, partial, st)
-                                   : launch_wtile<RtMat>(r, map, a, m->dev, partial, st);
+    const bool ok = m->specialized ? launch_wtile<T1Mat>(r, p.tw, map, a, m->dev, partial, st)
+                                   : launch_wtile<RtMat>(r, p.tw, map, a, m->dev, partial, st);
     if (!ok) return false;
     count_launch();
     if ((*status = launch_status()) != ADCT_OK) return true;
