@@ -165,6 +165,129 @@ def run_reference(args):
     return 0
 
 
+def _timed(fn, steps, warmup, stream, dev):
+    """Mean CUDA-event time (ms) of fn() over `steps` launches after `warmup` (one stream)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk:
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / steps, clk.summary()
+
+
+def run_config(args):
+    """Secondary BASELINE.json configurations (parity-test workloads, reported for evidence; the
+    driver's headline line is config 4).  One JSON line per (config, matrix)."""
+    import oracle
+    from oracle import matrices as OM
+    from paper_1808_02950_b200 import adct, catalog
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    hbm_peak, peak_kind = peaks()
+    lines = []
+
+    def emit(cfg, matrix, ms, blocks, bytes_per_block, bound, clk, cpu, extra=None):
+        achieved = blocks * bytes_per_block / (ms * 1e-3) / 1e9
+        line = {"metric": METRIC, "value": blocks / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f32",
+                "data": "synthetic", "config": {"workload": cfg, "matrix": matrix},
+                "roofline": {"bound": bound, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                             "bytes_per_block": bytes_per_block},
+                "clocks": clk, "cpu_baseline": cpu}
+        if extra:
+            line.update(extra)
+        print(json.dumps(line), flush=True)
+        lines.append(line)
+
+    def cpu_rate(fn, blocks):
+        t0 = time.perf_counter()
+        fn()
+        return {"value": blocks / (time.perf_counter() - t0), "unit": UNIT, "cores": oracle.num_threads(),
+                "kind": "oracle"}
+
+    if args.config in ("C3", "all"):
+        n = 1024
+        imgs = synth.ar1_stack(n, 1080, 1920, 0.95, seed=3, device=dev, noise_uniform=4.0, batch=16)
+        m = adct.Matrix.from_int(catalog.T1, "T1")
+        q = torch.empty((n, 135, 240, 8, 8), dtype=torch.int16, device=dev)
+        ms, clk = _timed(lambda: adct.approx_dct8x8_fwd_quant(m, imgs, 16, q=q, stream=stream), args.steps,
+                         args.warmup, stream, dev)
+        blocks = n * 135 * 240
+        nb, _ = oracle.row_scaling(OM.T1)
+        smp = imgs[:2].cpu().numpy()
+        cpu = cpu_rate(lambda: oracle.quantize(oracle.forward_int(OM.T1, smp), nb, 16), 2 * 135 * 240)
+        cpu["sample"] = "first 2 frames, by-definition forward + exact-integer quantiser"
+        ok = bool(np.array_equal(q[:2].cpu().numpy(), oracle.quantize(oracle.forward_int(OM.T1, smp), nb, 16)))
+        emit("C3: 1024 frames 1920x1080 u8 AR(1) rho=0.95 + U(-4,4), forward T1 with S folded into a step-16 "
+             "quantiser -> int16 block-major", "T1", ms, blocks, 192, "hbm", clk, cpu, {"parity_first_2_frames": ok})
+        del imgs, q
+    if args.config in ("C5", "all"):
+        nblk = 1 << args.c5_log2
+        x = synth.laplace_blocks(nblk, seed=5, device=dev).reshape(nblk, 8, 8)
+        rec = torch.empty_like(x)
+        for name in ("T1", "DCT"):
+            m = adct.Matrix.from_int(catalog.T1, "T1") if name == "T1" else adct.Matrix.from_real(
+                catalog.exact_dct(), "DCT")
+            ms, clk = _timed(lambda: adct.approx_dct8x8_roundtrip(m, x, 64, torch.int16, recon=rec, stream=stream),
+                             args.steps, args.warmup, stream, dev)
+            ok = bool(torch.equal(rec, x))
+            xs = x[:1 << 14].cpu().numpy()
+            if name == "T1":
+                n_, s_ = oracle.row_scaling(OM.T1)
+                g_, _ = oracle.synthesis_matrix(oracle.chat_from_int(OM.T1))
+                fn = lambda: oracle.inverse(g_, oracle.scale(oracle.forward_int(OM.T1, xs), s_))  # noqa: E731
+            else:
+                g_, _ = oracle.synthesis_matrix(OM.C)
+                fn = lambda: oracle.inverse(g_, oracle.forward_real(OM.C, xs))  # noqa: E731
+            cpu = cpu_rate(fn, 1 << 14)
+            cpu["sample"] = "2^14 blocks, by-definition forward + inverse"
+            emit(f"C5: 2^{args.c5_log2} int16 Laplace(10) blocks, fused forward + inverse (r=64) -> int16, "
+                 f"in-place-sized out-of-place", name, ms, nblk, 256, "hbm", clk, cpu,
+                 {"roundtrip_bit_exact": ok})
+        del x, rec
+    if args.config in ("C1", "C2", "all"):
+        rs = list(range(1, 65))
+        if args.config in ("C1", "all"):
+            img = synth.ar1_field(1, 512, 512, 0.95, seed=1).to(dev)
+            m = adct.Matrix.from_int(catalog.T1, "T1")
+            ws = torch.empty(adct.workspace_bytes(adct.geom_of(img), 64), dtype=torch.uint8, device=dev)
+            out = torch.empty((1, 64), dtype=torch.float64, device=dev)
+            ms, clk = _timed(lambda: adct.approx_dct8x8_fused_sse(m, img, rs, workspace=ws, sse=out, stream=stream),
+                             args.steps, args.warmup, stream, dev)
+            cpu = cpu_rate(lambda: oracle.codec_sse(img.cpu().numpy(), rs, t=OM.T1), 4096)
+            cpu["sample"] = "the same image, r = 1..64"
+            emit("C1: one 512x512 AR(1) image, T1, fwd -> retain r -> inv -> PSNR for every r = 1..64", "T1", ms,
+                 4096, 64, "latency", clk, cpu)
+        if args.config in ("C2", "all"):
+            rho, std = synth.config2_params(45, 2)
+            imgs = synth.ar1_stack(45, 512, 512, rho, std=std, seed=2, device=dev, batch=15)
+            ws = torch.empty(adct.workspace_bytes(adct.geom_of(imgs), 64), dtype=torch.uint8, device=dev)
+            out = torch.empty((45, 64), dtype=torch.float64, device=dev)
+            mats = [adct.Matrix.from_real(catalog.exact_dct(), "DCT") if nm == "DCT" else
+                    adct.Matrix.from_int(catalog.INTEGER[nm], nm) for nm in catalog.CONFIG2_ORDER]
+
+            def all9():
+                for mm in mats:
+                    adct.approx_dct8x8_fused_sse(mm, imgs, rs, workspace=ws, sse=out, stream=stream)
+
+            ms, clk = _timed(all9, args.steps, args.warmup, stream, dev)
+            smp = imgs[:1].cpu().numpy()
+            cpu = cpu_rate(lambda: oracle.codec_sse(smp, rs, t=OM.T1), 4096)
+            cpu["sample"] = "image 0, T1, r = 1..64"
+            emit("C2: 45 AR(1) 512x512 images, r = 1..64 curves for the 9 matrices (T1, C, T2, LO, SDCT, RDCT, "
+                 "BAS-2008b, T4, T6) through the same kernel; value counts block x matrix", "all 9", ms,
+                 45 * 4096 * 9, 64, "alu", clk, cpu)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -174,11 +297,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "all"],
+                    help="secondary BASELINE.json configuration instead of the config-4 headline")
+    ap.add_argument("--c5-log2", type=int, default=26)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
     if args.warmup < 3:
         args.warmup = 3
+    if args.config:
+        return run_config(args)
 
     from paper_1808_02950_b200 import adct, catalog, parallel
 

@@ -139,6 +139,17 @@ adct_status psnr_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
 
 /* --- fused performance paths (must equal the composition of the calls above) ----------- */
 
+/* Forward -> zonal retention (first r in zig-zag order) -> inverse, written as a
+ * reconstruction, with each block read once and its coefficients kept in registers: the
+ * composition approx_dct8x8_fwd -> zonal_retain -> approx_dct8x8_inv (
+ * BASELINE.json config 5 runs it at r = 64 on int16 residual blocks).  src: device, U8 or
+ * I16 samples with geometry g (8-byte / 16-byte aligned rows); recon: device, same geometry,
+ * dtype recon_t with the clip policy of approx_dct8x8_inv, except that the clip range is the
+ * source's sample range ([0,255] for U8, [-32768,32767] for I16).  r in 1..64 else
+ * ADCT_E_INVALID_ARGUMENT.  Any matrix (integer or real). */
+adct_status approx_dct8x8_roundtrip(const adct_matrix* m, const void* src, adct_dtype src_t, adct_geom g, int32_t r,
+                                    void* recon, adct_dtype recon_t, adct_clip clip, void* stream);
+
 /* Forward -> retain r -> inverse -> clip -> per-image SSE for every r in r_list, reading
  * each block once.  r_list: HOST array of n_r values in 1..64 (n_r <= 64).
  * sse: device fp64 [n_images][n_r].  workspace >= adct_workspace_bytes(g, n_r). */

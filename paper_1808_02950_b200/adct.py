@@ -28,6 +28,7 @@ SYMBOLS = [
     "adct_zigzag_order", "approx_dct8x8_fwd", "zonal_retain", "approx_dct8x8_inv", "psnr_reduce",
     "approx_dct8x8_fused_sse", "adct_host_workspace_bytes", "approx_dct8x8_fused_sse_host",
     "approx_dct8x8_fwd_quant", "adct_workspace_bytes", "adct_status_str", "adct_launch_count",
+    "approx_dct8x8_roundtrip",
 ]
 
 
@@ -64,6 +65,7 @@ def _load() -> ctypes.CDLL:
     L.adct_host_workspace_bytes.restype = ctypes.c_size_t
     L.approx_dct8x8_fused_sse_host.argtypes = [P, P, S, Geom, P, I32_, S, P, I64_, P, ctypes.c_size_t, P]
     L.approx_dct8x8_fwd_quant.argtypes = [P, P, Geom, I32_, P, P]
+    L.approx_dct8x8_roundtrip.argtypes = [P, P, S, Geom, I32_, P, S, S, P]
     L.adct_workspace_bytes.argtypes = [Geom, I32_]
     L.adct_workspace_bytes.restype = ctypes.c_size_t
     L.adct_status_str.argtypes = [S]
@@ -243,6 +245,24 @@ def psnr_reduce(orig: torch.Tensor, recon: torch.Tensor, peak: float = 255.0, cl
 
 
 # ---- fused paths ------------------------------------------------------------------------------
+
+def approx_dct8x8_roundtrip(m: Matrix, src: torch.Tensor, r: int = 64, recon_dtype=torch.int16,
+                            clip: int | None = None, recon: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Forward -> retain r -> inverse of every block of src [n, H, W] in one pass; the
+    reconstruction has src's shape and strides (int16/uint8: rounded and saturated)."""
+    if clip is None:
+        clip = CLIP_ROUND if recon_dtype in (torch.int16, torch.uint8) else CLIP_NONE
+    g = geom_of(src)
+    if recon is None:
+        recon = torch.empty_strided(tuple(src.shape[-3:]) if src.dim() == 3 else tuple(src.shape),
+                                    src.stride(), dtype=recon_dtype, device=src.device)
+    if tuple(recon.stride()) != tuple(src.stride()):
+        raise ValueError("recon must have the strides of src")
+    _check(lib.approx_dct8x8_roundtrip(m.handle, src.data_ptr(), dtype_code(src), g, int(r), recon.data_ptr(),
+                                       dtype_code(recon), int(clip), _stream_ptr(stream)),
+           "approx_dct8x8_roundtrip")
+    return recon
+
 
 def approx_dct8x8_fused_sse(m: Matrix, src: torch.Tensor, r_list, clip: int = CLIP_NONE,
                             workspace: torch.Tensor | None = None, sse: torch.Tensor | None = None,

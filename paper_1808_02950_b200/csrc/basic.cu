@@ -181,6 +181,47 @@ __global__ void __launch_bounds__(256) inv_kernel(const CoefT* __restrict__ coef
   }
 }
 
+// ---- fused round trip: forward -> zonal retention -> inverse -> reconstruction --------------------
+// The composition approx_dct8x8_fwd -> zonal_retain -> approx_dct8x8_inv in one pass (config 5:
+// forward + inverse of int16 residual blocks): each block is read once and its reconstruction
+// written once; the coefficients never leave registers.  wk[k*8+l] = the inverse weight of the
+// coefficient times its zig-zag keep bit (0 for dropped coefficients).
+struct Wk {
+  float w[64];
+};
+
+template <typename SrcT, class MP>
+__global__ void __launch_bounds__(256) roundtrip_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm, Wk wk,
+                                                        FastDiv dnbi, FastDiv dbw, uint32_t nblocks, int out_t,
+                                                        int clip, float lo, float hi, void* __restrict__ recon) {
+  const MP m(dm);
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += gridDim.x * blockDim.x) {
+    float x[8][8], y[8][8];
+    load_block(src, g, b, dnbi, dbw, x);
+    fwd2d(m, x, y);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int l = 0; l < 8; ++l) y[k][l] *= wk.w[k * 8 + l];
+    inv2d<MP, ~0ull>(m, y, x);
+    const uint32_t img = fdiv(b, dnbi);
+    const uint32_t q = b - img * g.nbi;
+    const uint32_t by = fdiv(q, dbw);
+    const uint32_t bx = q - by * g.bw;
+    const int64_t off = (int64_t)img * g.image_stride + (int64_t)by * 8 * g.row_stride + (int64_t)bx * 8;
+    if (out_t == ADCT_F32) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) store_row<float>((float*)recon + off + (int64_t)i * g.row_stride, x[i], clip, lo, hi);
+    } else if (out_t == ADCT_I16) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) store_row<int16_t>((int16_t*)recon + off + (int64_t)i * g.row_stride, x[i], clip, lo, hi);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) store_row<uint8_t>((uint8_t*)recon + off + (int64_t)i * g.row_stride, x[i], clip, lo, hi);
+    }
+  }
+}
+
 // ---- per-image squared error (deterministic two-level reduction) ------------------------------
 template <typename T>
 __device__ __forceinline__ float sample_at(const T* p) { return (float)*p; }
@@ -368,6 +409,42 @@ adct_status approx_dct8x8_inv(const adct_matrix* m, const void* coef, adct_dtype
   if (coef_t == ADCT_I16) { ADCT_INV_DISPATCH(int16_t) }
   ADCT_INV_DISPATCH(float)
 #undef ADCT_INV_DISPATCH
+}
+
+adct_status approx_dct8x8_roundtrip(const adct_matrix* m, const void* src, adct_dtype src_t, adct_geom g, int32_t r,
+                                    void* recon, adct_dtype recon_t, adct_clip clip, void* stream) {
+  if (!m || !src || !recon) return ADCT_E_INVALID_ARGUMENT;
+  if (adct_status s = check_geom(g)) return s;
+  if (src_t != ADCT_U8 && src_t != ADCT_I16) return ADCT_E_INVALID_ARGUMENT;
+  if (r < 1 || r > 64) return ADCT_E_INVALID_ARGUMENT;
+  if (clip != ADCT_CLIP_NONE && clip != ADCT_CLIP && clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  if (recon_t == ADCT_U8 || recon_t == ADCT_I16) {
+    if (clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  } else if (recon_t != ADCT_F32) {
+    return ADCT_E_INVALID_ARGUMENT;
+  }
+  if (!aligned(src, src_t == ADCT_U8 ? 8 : 16) || !aligned(recon, recon_t == ADCT_U8 ? 8 : 16)) return ADCT_E_ALIGNMENT;
+  const KGeom kg = make_kgeom(g);
+  const uint32_t nb = (uint32_t)(g.n_images * kg.nbi);
+  if (nb == 0) return ADCT_OK;
+  Wk wk;
+  const uint64_t keep = keep_mask(r);
+  for (int p = 0; p < 64; ++p) wk.w[p] = ((keep >> p) & 1ull) ? (m->is_int ? m->dev.wy[p] : m->dev.wb[p]) : 0.0f;
+  const float lo = src_t == ADCT_U8 ? 0.0f : -32768.0f, hi = src_t == ADCT_U8 ? 255.0f : 32767.0f;
+  const FastDiv dnbi = make_fastdiv(kg.nbi), dbw = make_fastdiv(kg.bw);
+  const unsigned grid = grid_for(nb, 256, 8);
+  cudaStream_t st = (cudaStream_t)stream;
+#define ADCT_RT(T, MP)                                                                                       \
+  roundtrip_kernel<T, MP><<<grid, 256, 0, st>>>((const T*)src, kg, m->dev, wk, dnbi, dbw, nb, (int)recon_t, \
+                                                (int)clip, lo, hi, recon)
+  if (src_t == ADCT_U8) {
+    if (m->specialized) ADCT_RT(uint8_t, T1Mat); else ADCT_RT(uint8_t, RtMat);
+  } else {
+    if (m->specialized) ADCT_RT(int16_t, T1Mat); else ADCT_RT(int16_t, RtMat);
+  }
+#undef ADCT_RT
+  count_launch();
+  return launch_status();
 }
 
 adct_status psnr_reduce(const void* orig, adct_dtype orig_t, const void* recon, adct_dtype recon_t, adct_geom g,

@@ -291,3 +291,60 @@ def test_quantiser_exhaustive_values(mats):
         q = adct.approx_dct8x8_fwd_quant(mats["T1"], img.to(DEV), 16).cpu().numpy()
         n, s = oracle.row_scaling(M.T1)
         assert np.array_equal(q, oracle.quantize(oracle.forward_int(M.T1, img.numpy()), n, 16))
+
+
+# --- fused round trip (fwd -> retain -> inv in one pass; config 5) ---------------------------------
+
+def _oracle_recon(name, img, r):
+    """Oracle reconstruction image of fwd -> retain r -> inverse (no clip)."""
+    if name == "DCT":
+        chat = M.C
+        bp = oracle.retain(oracle.forward_real(M.C, img), r)
+    else:
+        chat = oracle.chat_from_int(tmat(name))
+        n, s = oracle.row_scaling(tmat(name))
+        bp = oracle.scale(oracle.retain(oracle.forward_int(tmat(name), img), r), s)
+    g, _ = oracle.synthesis_matrix(chat)
+    return blocks_to_image(oracle.inverse(g, bp))
+
+
+@pytest.mark.parametrize("name", ["T1", "T6", "LO", "SDCT", "BAS-2008b", "DCT"])
+@pytest.mark.parametrize("r", [1, 10, 33, 64])
+@pytest.mark.parametrize("kind", ["ar1", "laplace"])
+def test_roundtrip_f32_matches_composition(mats, name, r, kind):
+    img = images(kind, 2, 40, 72, seed=50 + r)
+    rec = adct.approx_dct8x8_roundtrip(mats[name], img.to(DEV), r, torch.float32).cpu().numpy()
+    ref = _oracle_recon(name, img.numpy(), r)
+    assert rel_block_err(rec, ref) <= RTOL
+
+
+@pytest.mark.parametrize("name", ["T1", "DCT"])
+def test_roundtrip_config5_int16_bit_exact(mats, name):
+    """C5 pin: rint(inverse(forward(X))) == X at r = 64 for int16 Laplace blocks,
+    here through the fused one-pass kernel, with a ragged tail of blocks."""
+    n_blocks = (1 << 16) + 37
+    x = synth.laplace_blocks(n_blocks, seed=5).reshape(n_blocks, 8, 8)
+    rec = adct.approx_dct8x8_roundtrip(mats[name], x.to(DEV), 64, torch.int16)
+    assert torch.equal(rec.cpu(), x)
+
+
+def test_roundtrip_u8_round_clip_and_strided(mats):
+    img = images("ar1", 2, 48, 80, seed=7)
+    big = torch.zeros((2, 56, 96), dtype=torch.uint8)
+    big[:, 8:56, 16:96] = img
+    view = big.to(DEV)[:, 8:56, 16:96]
+    rec = adct.approx_dct8x8_roundtrip(mats["T1"], view, 10, torch.uint8).cpu().numpy()
+    ref = _oracle_recon("T1", img.numpy(), 10)
+    ref_u8 = np.clip(np.rint(ref), 0, 255)
+    diff = np.abs(rec.astype(np.int64) - ref_u8)
+    assert diff.max() <= 1
+    assert np.all(np.abs(np.abs(ref - np.floor(ref)) - 0.5)[diff > 0] < 1e-3)
+
+
+def test_roundtrip_argument_errors(mats):
+    x = torch.zeros((1, 8, 8), dtype=torch.int16, device=DEV)
+    for bad_r in (0, 65):
+        with pytest.raises(adct.AdctError):
+            adct.approx_dct8x8_roundtrip(mats["T1"], x, bad_r, torch.int16)
+    with pytest.raises(adct.AdctError):  # integer output needs CLIP_ROUND
+        adct.approx_dct8x8_roundtrip(mats["T1"], x, 10, torch.int16, clip=adct.CLIP_NONE)
