@@ -292,6 +292,10 @@ void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, in
 
 }  // namespace adct
 
+namespace adct {
+bool roundtrip_blockmajor(const adct_matrix* m, const void* src, const adct_geom& g, const float* wk_in, void* recon,
+                          adct_dtype recon_t, adct_clip clip, float lo, float hi, cudaStream_t st, adct_status* status);
+}
 using namespace adct;
 
 namespace {
@@ -431,9 +435,13 @@ adct_status approx_dct8x8_roundtrip(const adct_matrix* m, const void* src, adct_
   const uint64_t keep = keep_mask(r);
   for (int p = 0; p < 64; ++p) wk.w[p] = ((keep >> p) & 1ull) ? (m->is_int ? m->dev.wy[p] : m->dev.wb[p]) : 0.0f;
   const float lo = src_t == ADCT_U8 ? 0.0f : -32768.0f, hi = src_t == ADCT_U8 ? 255.0f : 32767.0f;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (src_t == ADCT_I16) {  // block-major int16 stacks (config 5): TMA-streamed kernel
+    adct_status bs = ADCT_OK;
+    if (roundtrip_blockmajor(m, src, g, wk.w, recon, recon_t, clip, lo, hi, st, &bs)) return bs;
+  }
   const FastDiv dnbi = make_fastdiv(kg.nbi), dbw = make_fastdiv(kg.bw);
   const unsigned grid = grid_for(nb, 256, 8);
-  cudaStream_t st = (cudaStream_t)stream;
 #define ADCT_RT(T, MP)                                                                                       \
   roundtrip_kernel<T, MP><<<grid, 256, 0, st>>>((const T*)src, kg, m->dev, wk, dnbi, dbw, nb, (int)recon_t, \
                                                 (int)clip, lo, hi, recon)

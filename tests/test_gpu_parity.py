@@ -348,3 +348,22 @@ def test_roundtrip_argument_errors(mats):
             adct.approx_dct8x8_roundtrip(mats["T1"], x, bad_r, torch.int16)
     with pytest.raises(adct.AdctError):  # integer output needs CLIP_ROUND
         adct.approx_dct8x8_roundtrip(mats["T1"], x, 10, torch.int16, clip=adct.CLIP_NONE)
+
+
+@pytest.mark.parametrize("name", ["T1", "DCT", "T6"])
+@pytest.mark.parametrize("out", [torch.int16, torch.float32])
+def test_roundtrip_blockmajor_tma_path(mats, name, out):
+    """Block-major int16 stacks with a multiple of 32 blocks take the TMA-streamed kernel:
+    int16 output bit-exact at r = 64 (C5 pin), fp32 output against the oracle at r = 10."""
+    n_blocks = 1 << 14
+    x = synth.laplace_blocks(n_blocks, seed=8).reshape(n_blocks, 8, 8)
+    xd = x.to(DEV)
+    if out == torch.int16:
+        rec = adct.approx_dct8x8_roundtrip(mats[name], xd, 64, torch.int16)
+        if name in ("T1", "DCT"):
+            assert torch.equal(rec.cpu(), x)
+        ref = np.rint(_oracle_recon(name, x.numpy(), 64))
+        assert np.abs(rec.cpu().numpy().astype(np.int64) - ref).max() <= 1
+    else:
+        rec = adct.approx_dct8x8_roundtrip(mats[name], xd, 10, torch.float32).cpu().numpy()
+        assert rel_block_err(rec, _oracle_recon(name, x.numpy(), 10)) <= RTOL
