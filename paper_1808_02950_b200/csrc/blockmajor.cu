@@ -13,6 +13,7 @@
 // which owns the block in tile row l, reads and writes its 16-byte rows at chunk (i ^ (l & 7)):
 // conflict-free shared-memory access with one thread per block.
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "adct_host.h"
@@ -46,6 +47,14 @@ __device__ __forceinline__ uint32_t f2_to_i16x2(float a, float b) {
 struct Wk {
   float w[64];
 };
+
+// byte of w as fp32 32768 + x (one PRMT; see stream.cu pxf)
+template <uint32_t SEL>
+__device__ __forceinline__ float pxf_q(uint32_t w, uint32_t magic) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(magic), "n"(SEL));
+  return __uint_as_float(r);
+}
 
 // ---- config 5: block-major round trip ----------------------------------------------------------
 // One tile = 32 consecutive blocks (4 KB of int16), one block per lane.  Output tile: 32 rows of
@@ -159,6 +168,175 @@ bool enc2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, uint64_t inner,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// ---- config 3: forward + uniform quantiser, u8 image tiles -> int16 block-major --------------
+// q_kl = round_half_away(Y_kl / c_kl), c_kl = step sqrt(n_k n_l) (reading A10).  Fast path per
+// coefficient: v = Y * (1/c) in fp32 (|error| < 2e-5 for |Y| < 2^17), 1.5*2^23 + v rounds it to
+// the nearest integer (the low 16 bits of the pattern are that integer in two's complement),
+// and the exact rounding remainder d = v - round(v) (Fast2Sum) flags coefficients within 2^-14
+// of a rounding boundary — every exact tie included — for which the block takes the exact
+// integer rule (2m-1)^2 P <= 4 Y^2 < (2m+1)^2 P, P = step^2 n_k n_l (fp64, exact below 2^53).
+struct QTab {
+  float inv[64];    // fp32(1 / c_kl)
+  double p[64];     // P_kl = step^2 n_k n_l
+};
+
+constexpr int kQWarps = 12;                 // 16 KB of shared memory per warp
+constexpr int kQInSlots = 2;
+
+__host__ __device__ constexpr bool t1_rational(int k, int l) {
+  return ((k & 3) == 2) == ((l & 3) == 2);
+}
+__host__ __device__ constexpr int t1_sqrt_nn(int k, int l) {  // sqrt(n_k n_l) where it is an integer
+  return ((k & 3) == 2) ? 20 : ((k & 3) == 0 ? ((l & 3) == 0 ? 8 : 12) : ((l & 3) == 0 ? 12 : 18));
+}
+
+template <int TW>
+__global__ void __launch_bounds__(32 * kQWarps, 1)
+    fwd_quant_tma_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                         QTab qt, float stepf, int32_t tpb, int32_t tpi, int32_t bh, uint32_t n_tiles, FastDiv dtpi,
+                         FastDiv dtpb, uint32_t magic) {
+  using MP = T1Mat;
+  const DevMat dm{};
+  constexpr int RT = 4096 / TW;  // rows per input tile
+  constexpr int BPR = TW / 8;    // blocks per band segment
+  constexpr int NB = RT / 8;     // bands per tile (2 or 4)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t wbase = smem_u32(smem) + (uint32_t)w * (kQInSlots * 4096 + 8192);
+  const uint32_t outb = wbase + kQInSlots * 4096;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kQWarps * (kQInSlots * 4096 + 8192)) + w * kQInSlots;
+  if (lane == 0) {
+    for (int i = 0; i < kQInSlots; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const MP m(dm);
+  const uint32_t wid = blockIdx.x * kQWarps + w, nw = gridDim.x * kQWarps;
+  // tile t -> (image, tile row, slice)
+  auto where = [&](uint32_t t, uint32_t& img, int32_t& trow, int32_t& slice) {
+    img = fdiv(t, dtpi);
+    const uint32_t r = t - img * (uint32_t)tpi;
+    trow = (int32_t)fdiv(r, dtpb);
+    slice = (int32_t)r - trow * tpb;
+  };
+  uint32_t pt = wid;
+  auto issue = [&](int slot) {
+    if (lane == 0) {
+      uint32_t img;
+      int32_t trow, slice;
+      where(pt, img, trow, slice);
+      mbar_arrive_expect_tx(&bars[slot], 4096u);
+      tma_load_3d(wbase + slot * 4096, &tin, slice * TW, trow * RT, (int32_t)img, smem_u32(&bars[slot]));
+    }
+    pt += nw;
+  };
+  for (int s = 0; s < kQInSlots; ++s)
+    if (pt < n_tiles) issue(s);
+  const uint32_t grp = (uint32_t)(lane / BPR), pos = (uint32_t)(lane % BPR);
+  const uint32_t lane_in = (uint32_t)pos * 8u + grp * 16u * TW;
+  int slot = 0;
+  uint32_t phase = 0;
+  for (uint32_t t = wid; t < n_tiles; t += nw) {
+    mbar_wait(&bars[slot], phase);
+    uint2 rows[2][8];
+    const uint32_t ib = wbase + slot * 4096 + lane_in;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rows[b][i] = lds64(ib + (uint32_t)(b * 8 + i) * TW);
+    __syncwarp();
+    fence_proxy_async();
+    if (pt < n_tiles) issue(slot);
+    if (++slot == kQInSlots) { slot = 0; phase ^= 1u; }
+    if (lane == 0) bulk_wait_read<0>();  // staging free once the previous tile's stores read it
+    __syncwarp();
+#pragma unroll 1
+    for (int b = 0; b < 2; ++b) {
+      float x[8][8], y[8][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        x[i][0] = pxf_q<0x7504u>(rows[b][i].x, magic); x[i][1] = pxf_q<0x7514u>(rows[b][i].x, magic);
+        x[i][2] = pxf_q<0x7524u>(rows[b][i].x, magic); x[i][3] = pxf_q<0x7534u>(rows[b][i].x, magic);
+        x[i][4] = pxf_q<0x7504u>(rows[b][i].y, magic); x[i][5] = pxf_q<0x7514u>(rows[b][i].y, magic);
+        x[i][6] = pxf_q<0x7524u>(rows[b][i].y, magic); x[i][7] = pxf_q<0x7534u>(rows[b][i].y, magic);
+      }
+      fwd2d(m, x, y);
+      // quantise.  T1: c_kl = step * sqrt(n_k n_l) is an integer multiple of step unless exactly
+      // one of k, l is in {2, 6} (n = 20 against 8 or 18); integer c is rounded exactly in fp32.
+      bool near = false;
+      uint32_t packed[32];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int l = 0; l < 8; l += 2) {
+          uint32_t u[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int kl = k * 8 + l + e;
+            const float yy = y[k][l + e] - (kl == 0 ? 64.0f * 32768.0f : 0.0f);  // exact
+            y[k][l + e] = yy;
+            if (t1_rational(k, l + e)) {
+              // |q| = floor((|Y| + c/2) / c): estimate, then the exact remainder decides
+              const float c = stepf * (float)t1_sqrt_nn(k, l + e);
+              const float A = fabsf(yy) + 0.5f * c;
+              const float f = A * qt.inv[kl] + 12582912.0f;
+              const float m0 = f - 12582912.0f;
+              const float rem = fmaf(-c, m0, A);
+              const float mf = rem < 0.0f ? m0 - 1.0f : m0;
+              const float qf = __uint_as_float(__float_as_uint(mf) | (__float_as_uint(yy) & 0x80000000u));
+              u[e] = __float_as_uint(qf + 12582912.0f);
+            } else {
+              const float v = yy * qt.inv[kl];
+              const float f = v + 12582912.0f;
+              near |= fabsf(v - (f - 12582912.0f)) > 0.49993896f;  // within 2^-14 of a boundary
+              u[e] = __float_as_uint(f);
+            }
+          }
+          packed[k * 4 + l / 2] = __byte_perm(u[0], u[1], 0x5410);
+        }
+      if (__any_sync(0xffffffffu, near)) {  // rare: exact integer rule at irrational positions
+#pragma unroll
+        for (int kl = 0; kl < 64; ++kl) {
+          if (t1_rational(kl >> 3, kl & 7)) continue;
+          const float yy = y[kl >> 3][kl & 7];
+          const float v = yy * qt.inv[kl];
+          const float f = v + 12582912.0f;
+          if (near && fabsf(v - (f - 12582912.0f)) > 0.49993896f) {
+            const double a2 = 4.0 * (double)yy * (double)yy, pp = qt.p[kl];
+            double mm = rint(fabs((double)yy) / sqrt(pp));
+            if (mm >= 1.0 && (2.0 * mm - 1.0) * (2.0 * mm - 1.0) * pp > a2) mm -= 1.0;
+            else if ((2.0 * mm + 1.0) * (2.0 * mm + 1.0) * pp <= a2) mm += 1.0;
+            const uint32_t q16 = (uint32_t)(uint16_t)(int16_t)(yy < 0.0f ? -(int)mm : (int)mm);
+            uint32_t& wv = packed[kl >> 1];
+            wv = (kl & 1) ? ((wv & 0xffffu) | (q16 << 16)) : ((wv & 0xffff0000u) | q16);
+          }
+        }
+      }
+      // staging: band segment (2*grp + b) rows of 128 B, swizzled by the row within the segment
+      const uint32_t ob = outb + (2u * grp + (uint32_t)b) * (uint32_t)BPR * 128u;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        sts128(ob + swz(pos, (uint32_t)k),
+               make_uint4(packed[k * 4], packed[k * 4 + 1], packed[k * 4 + 2], packed[k * 4 + 3]));
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      uint32_t img;
+      int32_t trow, slice;
+      where(t, img, trow, slice);
+#pragma unroll
+      for (int g = 0; g < NB; ++g) {
+        const int32_t band = trow * NB + g;
+        if (band < bh) tma_store_3d(&tout, 0, slice * BPR, (int32_t)img * bh + band, outb + (uint32_t)g * BPR * 128u);
+      }
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait<0>();
+}
+
 int g_bm_sms = 0;
 int bm_sms() {
   if (!g_bm_sms) {
@@ -187,7 +365,91 @@ adct_status launch_rt_bm(const CUtensorMap& tin, const CUtensorMap& tout, const 
   return ADCT_OK;
 }
 
+template <int TW>
+adct_status launch_quant(const CUtensorMap& tin, const CUtensorMap& tout, const QTab& qt, float stepf, int32_t tpb,
+                         int32_t tpi, int32_t bh, uint32_t n_tiles, cudaStream_t st) {
+  constexpr size_t smem = (size_t)kQWarps * (kQInSlots * 4096 + 8192) + kQWarps * kQInSlots * 8 + 1024;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [&] {
+    err = cudaFuncSetAttribute(fwd_quant_tma_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (err != cudaSuccess) return ADCT_E_CUDA;
+  const uint32_t need = (n_tiles + kQWarps - 1) / kQWarps;
+  const unsigned grid = (unsigned)(need < (uint32_t)bm_sms() ? need : (uint32_t)bm_sms());
+  fwd_quant_tma_kernel<TW><<<grid, 32 * kQWarps, smem, st>>>(tin, tout, qt, stepf, tpb, tpi, bh, n_tiles,
+                                                                  make_fastdiv((uint32_t)tpi),
+                                                                  make_fastdiv((uint32_t)tpb), 0x47000000u);
+  return ADCT_OK;
+}
+
 }  // namespace
+
+// TMA path of approx_dct8x8_fwd_quant (u8 images with 16-byte aligned strides, integer
+// matrices whose biased forward stays below 2^24).  Returns false when not applicable.
+bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t step, int16_t* q,
+                   cudaStream_t st, adct_status* status) {
+  if (!m->specialized) return false;  // the paper's T1 only (compile-time network and c_kl pattern)
+  if ((g.row_stride % 16) || (g.n_images > 1 && (g.image_stride % 16)) || !aligned(src, 16) || !aligned(q, 128))
+    return false;
+  if (step < 1 || step > 4096) return false;
+  // every intermediate of the forward on samples 2^15 + x must stay an exact fp32 integer
+  int64_t rs0 = 0;
+  for (int i = 0; i < 8; ++i) rs0 += std::llabs((long long)m->t[i]);
+  if ((double)m->max_u8 + 32768.0 * (double)(rs0 * rs0) >= 16777216.0) return false;
+  const int tw = [&] {
+    const int64_t t256 = ((g.width + 255) / 256) * ((g.height + 15) / 16);
+    const int64_t t128 = ((g.width + 127) / 128) * ((g.height + 31) / 32);
+    return (m->specialized && t128 < t256) ? 128 : 256;
+  }();
+  const int rows = 4096 / tw;
+  const int32_t tpb = (g.width + tw - 1) / tw;
+  const int32_t tpi = ((g.height + rows - 1) / rows) * tpb;
+  const int64_t n_tiles = g.n_images * (int64_t)tpi;
+  if (n_tiles >= ((int64_t)1 << 31)) return false;
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  CUtensorMap tin, tout;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)g.width, (cuuint64_t)g.height, (cuuint64_t)g.n_images};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.row_stride,
+                                   (cuuint64_t)(g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride)};
+    const cuuint32_t box[3] = {(cuuint32_t)tw, (cuuint32_t)rows, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(src), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  {
+    const int64_t bw = g.width / 8, bh = g.height / 8;
+    const cuuint64_t dims[3] = {64, (cuuint64_t)bw, (cuuint64_t)(g.n_images * bh)};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)(bw * 128)};
+    const cuuint32_t box[3] = {64, (cuuint32_t)(tw / 8), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tout, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, q, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  QTab qt;
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l) {
+      const double p = (double)step * step * (double)m->n[k] * (double)m->n[l];
+      qt.p[k * 8 + l] = p;
+      qt.inv[k * 8 + l] = (float)(1.0 / std::sqrt(p));
+    }
+  const int32_t bh = g.height / 8;
+  const float stepf = (float)step;
+  adct_status s = tw == 128 ? launch_quant<128>(tin, tout, qt, stepf, tpb, tpi, bh, (uint32_t)n_tiles, st)
+                            : launch_quant<256>(tin, tout, qt, stepf, tpb, tpi, bh, (uint32_t)n_tiles, st);
+  if (s == ADCT_OK) {
+    count_launch();
+    s = launch_status();
+  }
+  *status = s;
+  return true;
+}
 
 // Block-major fast path of approx_dct8x8_roundtrip: int16 source [n][8][8] contiguous, n a
 // multiple of 32, int16 or fp32 reconstruction with the same layout.  Returns false when not

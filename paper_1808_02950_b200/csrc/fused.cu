@@ -21,6 +21,8 @@ void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, in
 void launch_sweep_any(bool u8, bool specialized, int clip, dim3 grid, cudaStream_t st, const void* src,
                       const KGeom& kg, const DevMat& dm, const FastDiv& dbw, int32_t chunks, uint64_t rmask,
                       int32_t rmin, double* partial);
+bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t step, int16_t* q,
+                   cudaStream_t st, adct_status* status);
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
                      double* partial, cudaStream_t st, adct_status* status);
 
@@ -345,6 +347,10 @@ adct_status approx_dct8x8_fwd_quant(const adct_matrix* m, const uint8_t* src, ad
   const KGeom kg = make_kgeom(g);
   const uint32_t nb = (uint32_t)(g.n_images * kg.nbi);
   if (nb == 0) return ADCT_OK;
+  if (!g_disable_stream) {  // TMA-streamed kernel (u8 tiles in, swizzled int16 tiles out)
+    adct_status qs = ADCT_OK;
+    if (fwd_quant_tma(m, src, g, step, q, (cudaStream_t)stream, &qs)) return qs;
+  }
   DevMat dm = m->dev;
   for (int k = 0; k < 8; ++k)
     for (int l = 0; l < 8; ++l) {
