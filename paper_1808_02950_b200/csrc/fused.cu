@@ -18,9 +18,10 @@ namespace adct {
 
 void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
                      int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st);
-void launch_sweep_any(bool u8, bool specialized, int clip, dim3 grid, cudaStream_t st, const void* src,
-                      const KGeom& kg, const DevMat& dm, const FastDiv& dbw, int32_t chunks, uint64_t rmask,
-                      int32_t rmin, double* partial);
+void launch_sweep_any(bool u8, bool specialized, int clip, cudaStream_t st, const void* src, const adct_geom& g,
+                      const KGeom& kg, const DevMat& dm, const FastDiv& dbw, uint64_t rmask, int32_t rmin,
+                      double* partial);
+int64_t sweep_chunks(const adct_geom& g);
 bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t step, int16_t* q,
                    cudaStream_t st, adct_status* status);
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
@@ -210,8 +211,9 @@ adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geo
       if (r_list[i] < rmin) rmin = r_list[i];
       sm.s[i] = r_list[i] - 1;
     }
-    launch_sweep_any(std::is_same<SrcT, uint8_t>::value, MP::kConst, (int)clip, grid, st, s, kg, m->dev, dbw, chunks,
-                     rmask, rmin, partial);
+    launch_sweep_any(std::is_same<SrcT, uint8_t>::value, MP::kConst, (int)clip, st, s, g, kg, m->dev, dbw, rmask,
+                     rmin, partial);
+    chunks = (int32_t)sweep_chunks(g);
     slots = 64;
   }
   count_launch();

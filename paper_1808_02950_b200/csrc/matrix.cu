@@ -15,6 +15,8 @@
 namespace adct {
 std::atomic<int64_t> g_launches{0};
 
+int64_t sweep_chunks(const adct_geom& g);
+
 int64_t stream_stage_target() {
   static const int64_t v = [] {
     const char* e = std::getenv("ADCT_STREAM_STAGE_KB");
@@ -276,7 +278,7 @@ int64_t adct_launch_count(void) { return g_launches.load(); }
 
 size_t adct_workspace_bytes(adct_geom g, int32_t n_r) {
   (void)n_r;  // per-image partials hold all 64 r slots of the sweep kernel
-  const int64_t a = fused_chunks(g) * 64;
+  const int64_t a = (fused_chunks(g) > sweep_chunks(g) ? fused_chunks(g) : sweep_chunks(g)) * 64;
   const int64_t b = sse_chunks(g);
   const int64_t c = stream_partials_per_image(g);
   int64_t per = a > b ? a : b;

@@ -6,8 +6,7 @@
 namespace adct {
 namespace {
 
-constexpr int NT = kRedNT;
-constexpr int BPT = kFusedBPT;
+constexpr int NT = 32;  // one warp per CTA: small images still spread over every SM
 
 // ---- any list of r: incremental inverse of the dropped coefficients ----------------------
 // Coefficients are added in decreasing zig-zag rank z = 63..1; after adding rank z the
@@ -15,18 +14,16 @@ constexpr int BPT = kFusedBPT;
 // rank-one update e += (w y)_z h_k h_l^T (the inverse applied to one coefficient).
 template <typename SrcT, class MP>
 __global__ void __launch_bounds__(NT) fused_sweep_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm,
-                                                         FastDiv dbw, int32_t chunks, uint64_t rmask, int32_t rmin,
-                                                         int clip,
-                                                         double* __restrict__ partial) {
+                                                         FastDiv dbw, int32_t chunks, int32_t bpt, uint64_t rmask,
+                                                         int32_t rmin, int clip, double* __restrict__ partial) {
   __shared__ float zacc[64][NT];
-  __shared__ double red[NT / 32];
   const MP m(dm);
 #pragma unroll
   for (int z = 0; z < 64; ++z) zacc[z][threadIdx.x] = 0.0f;
   const SrcT* base = src + (int64_t)blockIdx.y * g.image_stride;
-  const uint32_t q0 = blockIdx.x * (NT * BPT) + threadIdx.x;
+  const uint32_t q0 = blockIdx.x * (NT * bpt) + threadIdx.x;
 #pragma unroll 1
-  for (int mb = 0; mb < BPT; ++mb) {
+  for (int mb = 0; mb < bpt; ++mb) {
     const uint32_t q = q0 + mb * NT;
     if (q >= g.nbi) break;
     typename Src<SrcT>::Row rows[8];
@@ -74,25 +71,38 @@ __global__ void __launch_bounds__(NT) fused_sweep_kernel(const SrcT* __restrict_
       }
     }
   }
-  __syncthreads();
-  // r = z+1 slots 0..62 (slot 63, r = 64, stays 0: nothing dropped)
+  __syncwarp();
+  // r = z+1 slots 0..62 (slot 63, r = 64, stays 0: nothing dropped); fixed shuffle order
+  double* out = partial + ((int64_t)blockIdx.y * chunks + blockIdx.x) * 64;
   for (int z = 0; z < 64; ++z) {
-    if (z == 63 || !((rmask >> (z + 1)) & 1ull)) {
-      if (threadIdx.x == 0) partial[((int64_t)blockIdx.y * chunks + blockIdx.x) * 64 + z] = 0.0;
-      continue;
-    }
-    const double tot = block_sum<NT>((double)zacc[z][threadIdx.x], red);
-    if (threadIdx.x == 0) partial[((int64_t)blockIdx.y * chunks + blockIdx.x) * 64 + z] = tot;
+    double v = (z == 63 || !((rmask >> (z + 1)) & 1ull)) ? 0.0 : (double)zacc[z][threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) out[z] = v;
   }
 }
 
 }  // namespace
 
-void launch_sweep_any(bool u8, bool specialized, int clip, dim3 grid, cudaStream_t st, const void* src,
-                      const KGeom& kg, const DevMat& dm, const FastDiv& dbw, int32_t chunks, uint64_t rmask,
-                      int32_t rmin, double* partial) {
+// blocks per thread of the sweep kernel: depends on the image size only, so that the partial
+// layout (and the summation order) is the same however the images are batched or sharded
+int32_t sweep_bpt(const adct_geom& g) {
+  const int64_t nbi = (int64_t)(g.height / 8) * (g.width / 8);
+  return nbi <= 65536 ? 1 : 8;
+}
+int64_t sweep_chunks(const adct_geom& g) {
+  const int64_t nbi = (int64_t)(g.height / 8) * (g.width / 8);
+  const int64_t per = (int64_t)NT * sweep_bpt(g);
+  return (nbi + per - 1) / per;
+}
+
+void launch_sweep_any(bool u8, bool specialized, int clip, cudaStream_t st, const void* src, const adct_geom& g,
+                      const KGeom& kg, const DevMat& dm, const FastDiv& dbw, uint64_t rmask, int32_t rmin,
+                      double* partial) {
+  const int32_t chunks = (int32_t)sweep_chunks(g), bpt = sweep_bpt(g);
+  const dim3 grid((unsigned)chunks, (unsigned)g.n_images);
 #define ADCT_SWEEP_C(T, MP) \
-  fused_sweep_kernel<T, MP><<<grid, NT, 0, st>>>((const T*)src, kg, dm, dbw, chunks, rmask, rmin, clip, partial);
+  fused_sweep_kernel<T, MP><<<grid, NT, 0, st>>>((const T*)src, kg, dm, dbw, chunks, bpt, rmask, rmin, clip, partial);
   if (u8) {
     if (specialized) { ADCT_SWEEP_C(uint8_t, T1Mat) } else { ADCT_SWEEP_C(uint8_t, RtMat) }
   } else {
