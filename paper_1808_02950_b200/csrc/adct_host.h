@@ -138,8 +138,12 @@ inline StreamPlan stream_plan(const adct_geom& g, int esz = 1) {
 // per-(chunk, warp) fp64 partials keep the per-image sums independent of the grid.
 constexpr int kWtWarps = 16;
 constexpr int kWtThreads = 32 * kWtWarps;
-constexpr int kWtSlots = 3;
-constexpr int kWtTileBytes = 4096;                  // 64 blocks: 2 per lane
+#ifndef ADCT_WT_BPL
+#define ADCT_WT_BPL 2
+#endif
+constexpr int kWtBPL = ADCT_WT_BPL;                 // blocks per lane per tile
+constexpr int kWtTileBytes = 2048 * kWtBPL;         // 32 * kWtBPL blocks of 64 bytes
+constexpr int kWtSlots = kWtBPL == 2 ? 3 : 2;       // ring depth (192 KB of shared memory)
 constexpr int kWtChunkTiles = kWtWarps * 8;         // 8 tiles per warp per chunk
 constexpr size_t kWtSmem = (size_t)kWtWarps * kWtSlots * kWtTileBytes + (size_t)kWtWarps * kWtSlots * 8 + 128;
 

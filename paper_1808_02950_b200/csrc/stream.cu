@@ -370,7 +370,7 @@ __device__ __forceinline__ bool wt_next(const WtArgs& a, int w, WtIt& it) {
 #ifndef ADCT_WT_UNROLL
 #define ADCT_WT_UNROLL 2
 #endif
-constexpr int kWtUnroll = ADCT_WT_UNROLL;  // unrolling of the 2-block loop (code size vs ILP)
+constexpr int kWtUnroll = ADCT_WT_UNROLL;  // unrolling of the per-lane block loop (code size vs ILP)
 
 template <class MP, int R, int TW>
 __global__ void __launch_bounds__(kWtThreads, 1)
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
                           uint32_t magic) {
   constexpr int RT = kWtTileBytes / TW;  // rows per tile
   constexpr int BPR = TW / 8;            // blocks per band in a tile = lanes per band group
+  static_assert(RT == 8 * kWtBPL * (32 / BPR), "tile shape");
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -409,44 +410,35 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   for (int s = 0; s < kWtSlots; ++s)
     if (pf.cg < a.n_chunks) issue(s);
 
-  // lane -> block column (lane % BPR) and its two bands 2*(lane / BPR), 2*(lane / BPR) + 1
-  const uint32_t lane_u32 = ring0 + (uint32_t)(lane % BPR) * 8u + (uint32_t)(lane / BPR) * 16u * TW;
+  // lane -> block column (lane % BPR) and its kWtBPL bands kWtBPL*(lane / BPR) + b
+  const uint32_t lane_u32 = ring0 + (uint32_t)(lane % BPR) * 8u + (uint32_t)(lane / BPR) * (8u * kWtBPL) * TW;
   int slot = 0;
   uint32_t phase = 0;
-  WtIt it;
-  it.cg = blockIdx.x;
-  wt_enter(a, w, it);
-  float acc = 0.0f;
-  // chunks in which this warp has no tile keep a zero partial
-  if (lane == 0)
-    for (uint32_t cz = blockIdx.x; cz < min(it.cg, a.n_chunks); cz += gridDim.x) partial[(int64_t)cz * kWtWarps + w] = 0.0;
-  while (it.cg < a.n_chunks) {
-    mbar_wait(&wfull[slot], phase);
-    const uint32_t p = lane_u32 + (uint32_t)slot * kWtTileBytes;
+  for (uint32_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
+    const uint32_t img = fdiv(cg, a.dcpi);
+    const int32_t n = min(kWtChunkTiles, a.tpi - (int32_t)(cg - img * (uint32_t)a.cpi) * kWtChunkTiles);
+    float acc = 0.0f;
+    for (int32_t j = w; j < n; j += kWtWarps) {  // this warp's tiles of the chunk
+      mbar_wait(&wfull[slot], phase);
+      const uint32_t p = lane_u32 + (uint32_t)slot * kWtTileBytes;
 #pragma unroll kWtUnroll
-    for (int b = 0; b < 2; ++b) {  // the lane's two blocks (consecutive bands of the tile)
-      uint2 rows[8];
+      for (int b = 0; b < kWtBPL; ++b) {  // the lane's blocks (consecutive bands of the tile)
+        uint2 rows[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)(b * 8 + i) * TW);
-      acc += block_sse_u8s<MP, R>(m, rows, magic);
-    }
-    __syncwarp();
-    // the slot was read through the generic proxy; order that before the async-proxy refill
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (pf.cg < a.n_chunks) issue(slot);
-    if (++slot == kWtSlots) { slot = 0; phase ^= 1u; }
-    const uint32_t cg = it.cg;
-    if (wt_next(a, w, it)) {  // chunk done: per-(chunk, warp) partial in a fixed shuffle order
-      double v = (double)acc;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) {
-        partial[(int64_t)cg * kWtWarps + w] = v;
-        for (uint32_t cz = cg + gridDim.x; cz < min(it.cg, a.n_chunks); cz += gridDim.x)
-          partial[(int64_t)cz * kWtWarps + w] = 0.0;
+        for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)(b * 8 + i) * TW);
+        acc += block_sse_u8s<MP, R>(m, rows, magic);
       }
-      acc = 0.0f;
+      __syncwarp();
+      // the slot was read through the generic proxy; order that before the async-proxy refill
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (pf.cg < a.n_chunks) issue(slot);
+      if (++slot == kWtSlots) { slot = 0; phase ^= 1u; }
     }
+    // per-(chunk, warp) partial in a fixed shuffle order (0 when the warp had no tile)
+    double v = (double)acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) partial[(int64_t)cg * kWtWarps + w] = v;
   }
 }
 
@@ -520,16 +512,17 @@ bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const 
                   cudaStream_t st) {
   if constexpr (!MP::kConst) {
     return r == 10 && launch_wtile_r<MP, 10>(tw, map, a, dm, partial, st);
-  }
-  switch (r) {
+  } else {
+    switch (r) {
 #define ADCT_WT_CASE(R) \
   case R:               \
     return launch_wtile_r<MP, R>(tw, map, a, dm, partial, st);
-    ADCT_WT_CASE(1) ADCT_WT_CASE(3) ADCT_WT_CASE(6) ADCT_WT_CASE(10) ADCT_WT_CASE(14)
-    ADCT_WT_CASE(15) ADCT_WT_CASE(21) ADCT_WT_CASE(28) ADCT_WT_CASE(36)
+      ADCT_WT_CASE(1) ADCT_WT_CASE(3) ADCT_WT_CASE(6) ADCT_WT_CASE(10) ADCT_WT_CASE(14)
+      ADCT_WT_CASE(15) ADCT_WT_CASE(21) ADCT_WT_CASE(28) ADCT_WT_CASE(36)
 #undef ADCT_WT_CASE
-    default:
-      return false;
+      default:
+        return false;
+    }
   }
 }
 
