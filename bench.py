@@ -253,6 +253,27 @@ def run_config(args):
                  f"in-place-sized out-of-place", name, ms, nblk, 256, "hbm", clk, cpu,
                  {"roundtrip_bit_exact": ok})
         del x, rec
+    if args.config in ("SSIM", "all"):
+        # next row f1: fused round trip (fwd -> retain r=14 -> inv, fp32 recon) then SSIM with
+        # 8x8 windows (reading A18) on the 512 luma frames of config 4
+        n = 128
+        y = synth.ar1_stack(n, 2160, 3840, 0.95, seed=4, device=dev, batch=8)
+        m = adct.Matrix.from_int(catalog.T1, "T1")
+        rec = torch.empty(y.shape, dtype=torch.float32, device=dev)
+        ws = torch.empty(adct.workspace_bytes(adct.geom_of(y), 1), dtype=torch.uint8, device=dev)
+
+        def ssim_step():
+            adct.approx_dct8x8_roundtrip(m, y, 14, torch.float32, recon=rec, stream=stream)
+            adct.ssim_reduce(y, rec, clip=adct.CLIP, workspace=ws, stream=stream)
+
+        ms, clk = _timed(ssim_step, args.steps, args.warmup, stream, dev)
+        from oracle import ssim as OS
+        smp = y[:1, :256, :256].cpu().numpy()
+        cpu = cpu_rate(lambda: OS.ssim(smp, smp), 32 * 32)
+        cpu["sample"] = "SSIM of one 256x256 crop (oracle windows)"
+        emit(f"SSIM (next row f1): {n} luma frames 3840x2160, T1 round trip r=14 -> fp32 recon -> SSIM 8x8 windows; "
+             "bytes/block = 64 in + 256 recon out + 64 + 256 re-read", "T1", ms, n * 270 * 480, 640, "hbm", clk, cpu)
+        del y, rec
     if args.config in ("C1", "C2", "all"):
         rs = list(range(1, 65))
         if args.config in ("C1", "all"):
@@ -297,7 +318,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "all"],
+    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "SSIM", "all"],
                     help="secondary BASELINE.json configuration instead of the config-4 headline")
     ap.add_argument("--c5-log2", type=int, default=26)
     args = ap.parse_args()

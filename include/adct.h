@@ -137,6 +137,19 @@ adct_status psnr_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
                         double peak, adct_clip clip, double* sse, double* psnr, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* Structural similarity per image (citing Wang et al. 2004; the paper prints no
+ * parameters — reading A18 in DESIGN.md, after SPEC S:L605): mean over every 8x8 window fully
+ * inside the image (stride 1, uniform weights) of
+ *   (2 mu_x mu_y + C1)(2 sigma_xy + C2) / ((mu_x^2 + mu_y^2 + C1)(sigma_x^2 + sigma_y^2 + C2)),
+ * C1 = (0.01 peak)^2, C2 = (0.03 peak)^2, population (1/64) statistics.  orig: ADCT_U8 or
+ * ADCT_I16; recon: ADCT_F32/ADCT_U8/ADCT_I16 with the same geometry; the clip policy (reading
+ * A6) is applied to recon with the range [0, peak].  ssim: device fp64 [n_images].  H, W >= 8,
+ * n_images <= 65535; workspace >= adct_workspace_bytes(g, 1).  Deterministic (fixed-order
+ * reductions). */
+adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, adct_dtype recon_t, adct_geom g,
+                        double peak, adct_clip clip, double* ssim, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
 /* --- fused performance paths (must equal the composition of the calls above) ----------- */
 
 /* Forward -> zonal retention (first r in zig-zag order) -> inverse, written as a

@@ -28,7 +28,7 @@ SYMBOLS = [
     "adct_zigzag_order", "approx_dct8x8_fwd", "zonal_retain", "approx_dct8x8_inv", "psnr_reduce",
     "approx_dct8x8_fused_sse", "adct_host_workspace_bytes", "approx_dct8x8_fused_sse_host",
     "approx_dct8x8_fwd_quant", "adct_workspace_bytes", "adct_status_str", "adct_launch_count",
-    "approx_dct8x8_roundtrip",
+    "approx_dct8x8_roundtrip", "ssim_reduce",
 ]
 
 
@@ -66,6 +66,7 @@ def _load() -> ctypes.CDLL:
     L.approx_dct8x8_fused_sse_host.argtypes = [P, P, S, Geom, P, I32_, S, P, I64_, P, ctypes.c_size_t, P]
     L.approx_dct8x8_fwd_quant.argtypes = [P, P, Geom, I32_, P, P]
     L.approx_dct8x8_roundtrip.argtypes = [P, P, S, Geom, I32_, P, S, S, P]
+    L.ssim_reduce.argtypes = [P, S, P, S, Geom, D, S, P, P, ctypes.c_size_t, P]
     L.adct_workspace_bytes.argtypes = [Geom, I32_]
     L.adct_workspace_bytes.restype = ctypes.c_size_t
     L.adct_status_str.argtypes = [S]
@@ -242,6 +243,23 @@ def psnr_reduce(orig: torch.Tensor, recon: torch.Tensor, peak: float = 255.0, cl
                            int(clip), sse.data_ptr(), psnr.data_ptr(), workspace.data_ptr(), workspace.numel(),
                            _stream_ptr(stream)), "psnr_reduce")
     return sse, psnr
+
+
+def ssim_reduce(orig: torch.Tensor, recon: torch.Tensor, peak: float = 255.0, clip: int = CLIP_NONE,
+                workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Mean SSIM (8x8 uniform windows, reading A18) per image, fp64 [n]."""
+    g = geom_of(orig)
+    gr = geom_of(recon)
+    if (gr.n_images, gr.height, gr.width, gr.row_stride) != (g.n_images, g.height, g.width, g.row_stride):
+        raise ValueError("orig and recon must share the geometry (strides in elements)")
+    out = torch.empty(g.n_images, dtype=torch.float64, device=orig.device)
+    nbytes = workspace_bytes(g, 1)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=orig.device)
+    _check(lib.ssim_reduce(orig.data_ptr(), dtype_code(orig), recon.data_ptr(), dtype_code(recon), g, float(peak),
+                           int(clip), out.data_ptr(), workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)),
+           "ssim_reduce")
+    return out
 
 
 # ---- fused paths ------------------------------------------------------------------------------

@@ -6,6 +6,7 @@
 // plus the config-3 forward+quantiser.  One thread owns one 8x8 block; grid-stride loops
 // sized in multiples of the SM count.
 #include <cmath>
+#include <mutex>
 
 #include "adct_host.h"
 
@@ -256,7 +257,8 @@ constexpr int kFinNT = 256;
 __global__ void __launch_bounds__(kFinNT) finalize_kernel(const double* __restrict__ partial, int32_t chunks,
                                                           int64_t n_images, int32_t slots, SlotMap slot_of,
                                                           int32_t n_out, double npix, double peak,
-                                                          double* __restrict__ sse, double* __restrict__ psnr) {
+                                                          double* __restrict__ sse, double* __restrict__ psnr,
+                                                          double scale) {
   __shared__ double red[kFinNT];
   const int64_t img = blockIdx.x;
   const int32_t o = blockIdx.y;
@@ -272,21 +274,113 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(const double* __restri
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const double tot = red[0];
+    const double tot = red[0] * scale;
     const int64_t t = img * n_out + o;
     sse[t] = tot;
     if (psnr) psnr[t] = tot == 0.0 ? INFINITY : 10.0 * log10(peak * peak / (tot / npix));
   }
 }
 
+// ---- SSIM (reading A18: 8x8 uniform windows, K1 = 0.01, K2 = 0.03, L = peak) -------------------
+// One CTA per 32x32 tile of window positions: the 39x39 samples of both images are staged in
+// shared memory, horizontal 8-sums of x, y, x^2, y^2, xy are formed per row, then vertical
+// 8-sums per position, all in fp64; per-CTA sums of the window SSIMs are reduced in a fixed
+// order and finalize_kernel averages an image's tiles in index order.
+constexpr int kSsimT = 32, kSsimIn = kSsimT + 7, kSsimNT = 256;
+
+template <typename OrigT, typename RecT>
+__global__ void __launch_bounds__(kSsimNT) ssim_kernel(const OrigT* __restrict__ orig, const RecT* __restrict__ rec,
+                                                       KGeom g, int32_t height, int32_t width, int32_t ntx,
+                                                       int32_t tiles, int clip, float lo, float hi, double c1,
+                                                       double c2, double* __restrict__ partial) {
+  extern __shared__ double ssm[];
+  float* sx = reinterpret_cast<float*>(ssm);                 // [39][40]
+  float* sy = sx + kSsimIn * 40;                             // [39][40]
+  double* hs = ssm + (kSsimIn * 40 * 2 + 1) / 2;             // [5][39][32]
+  __shared__ double red[kSsimNT / 32];
+  const uint32_t img = blockIdx.y;
+  const int32_t tx = (int32_t)blockIdx.x % ntx, ty = (int32_t)blockIdx.x / ntx;
+  const int32_t x0 = tx * kSsimT, y0 = ty * kSsimT;
+  const int64_t ibase = (int64_t)img * g.image_stride;
+  for (int i = threadIdx.x; i < kSsimIn * kSsimIn; i += kSsimNT) {
+    const int r = i / kSsimIn, c = i % kSsimIn;
+    const int yy = y0 + r, xx = x0 + c;
+    float a = 0.0f, b = 0.0f;
+    if (yy < height && xx < width) {
+      const int64_t off = ibase + (int64_t)yy * g.row_stride + xx;
+      a = (float)orig[off];
+      b = (float)rec[off];
+      if (clip != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
+      if (clip == ADCT_CLIP_ROUND) b = rintf(b);
+    }
+    sx[r * 40 + c] = a;
+    sy[r * 40 + c] = b;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSsimIn * kSsimT; i += kSsimNT) {
+    const int r = i / kSsimT, c = i % kSsimT;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double a = sx[r * 40 + c + k], b = sy[r * 40 + c + k];
+      s0 += a;
+      s1 += b;
+      s2 = fma(a, a, s2);
+      s3 = fma(b, b, s3);
+      s4 = fma(a, b, s4);
+    }
+    hs[0 * kSsimIn * kSsimT + i] = s0;
+    hs[1 * kSsimIn * kSsimT + i] = s1;
+    hs[2 * kSsimIn * kSsimT + i] = s2;
+    hs[3 * kSsimIn * kSsimT + i] = s3;
+    hs[4 * kSsimIn * kSsimT + i] = s4;
+  }
+  __syncthreads();
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kSsimT * kSsimT; i += kSsimNT) {
+    const int r = i / kSsimT, c = i % kSsimT;
+    if (y0 + r + 8 > height || x0 + c + 8 > width) continue;
+    double v[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += hs[q * kSsimIn * kSsimT + (r + k) * kSsimT + c];
+      v[q] = t * (1.0 / 64.0);
+    }
+    const double mx = v[0], my = v[1];
+    const double vx = v[2] - mx * mx, vy = v[3] - my * my, cxy = v[4] - mx * my;
+    acc += ((2.0 * mx * my + c1) * (2.0 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2));
+  }
+  const double tot = block_sum<kSsimNT>(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)img * tiles + blockIdx.x] = tot;
+}
+
+constexpr size_t kSsimSmem = (size_t)(kSsimIn * 40 * 2 + 1) / 2 * 8 + (size_t)5 * kSsimIn * kSsimT * 8;
+
 }  // namespace
+
+int64_t ssim_tiles(const adct_geom& g) {
+  if (g.height < 8 || g.width < 8) return 0;
+  return (int64_t)((g.width - 7 + kSsimT - 1) / kSsimT) * ((g.height - 7 + kSsimT - 1) / kSsimT);
+}
+
+void launch_finalize_scaled(const double* partial, int32_t chunks, int64_t n_images, double scale, double* out,
+                            cudaStream_t st) {
+  if (n_images == 0) return;
+  SlotMap sm{};
+  finalize_kernel<<<dim3((unsigned)n_images, 1u), kFinNT, 0, st>>>(partial, chunks, n_images, 1, sm, 1, 1.0, 1.0, out,
+                                                                   nullptr, scale);
+  count_launch();
+}
 
 // exported to fused.cu
 void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
                      int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st) {
   if (n_images * n_out == 0) return;
   finalize_kernel<<<dim3((unsigned)n_images, (unsigned)n_out), kFinNT, 0, st>>>(partial, chunks, n_images, slots,
-                                                                                slot_of, n_out, npix, peak, sse, psnr);
+                                                                                slot_of, n_out, npix, peak, sse, psnr,
+                                                                                1.0);
   count_launch();
 }
 
@@ -452,6 +546,53 @@ adct_status approx_dct8x8_roundtrip(const adct_matrix* m, const void* src, adct_
   }
 #undef ADCT_RT
   count_launch();
+  return launch_status();
+}
+
+adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, adct_dtype recon_t, adct_geom g,
+                        double peak, adct_clip clip, double* ssim, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  if (!orig || !recon || !ssim) return ADCT_E_INVALID_ARGUMENT;
+  if (adct_status s = check_geom(g)) return s;
+  if (orig_t != ADCT_U8 && orig_t != ADCT_I16) return ADCT_E_INVALID_ARGUMENT;
+  if (recon_t != ADCT_U8 && recon_t != ADCT_I16 && recon_t != ADCT_F32) return ADCT_E_INVALID_ARGUMENT;
+  if (clip != ADCT_CLIP_NONE && clip != ADCT_CLIP && clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  if (!(peak > 0.0)) return ADCT_E_INVALID_ARGUMENT;
+  if (!workspace || workspace_bytes < adct_workspace_bytes(g, 1)) return ADCT_E_WORKSPACE;
+  if (g.n_images == 0) return ADCT_OK;
+  if (g.n_images > 65535) return ADCT_E_INVALID_ARGUMENT;
+  cudaStream_t st = (cudaStream_t)stream;
+  const KGeom kg = make_kgeom(g);
+  const int32_t ntx = (g.width - 7 + kSsimT - 1) / kSsimT;
+  const int32_t tiles = (int32_t)ssim_tiles(g);
+  const float lo = 0.0f, hi = (float)peak;  // clip range of the reconstruction: [0, peak]
+  const double c1 = (0.01 * peak) * (0.01 * peak), c2 = (0.03 * peak) * (0.03 * peak);
+  double* partial = (double*)workspace;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(ssim_kernel<uint8_t, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
+    cudaFuncSetAttribute(ssim_kernel<uint8_t, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
+    cudaFuncSetAttribute(ssim_kernel<uint8_t, int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
+    cudaFuncSetAttribute(ssim_kernel<int16_t, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
+    cudaFuncSetAttribute(ssim_kernel<int16_t, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
+    cudaFuncSetAttribute(ssim_kernel<int16_t, int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
+  });
+  const dim3 grid((unsigned)tiles, (unsigned)g.n_images);
+#define ADCT_SSIM(OT, RT)                                                                                      \
+  ssim_kernel<OT, RT><<<grid, kSsimNT, kSsimSmem, st>>>((const OT*)orig, (const RT*)recon, kg, g.height, g.width, \
+                                                        ntx, tiles, (int)clip, lo, hi, c1, c2, partial)
+  if (orig_t == ADCT_U8) {
+    if (recon_t == ADCT_F32) ADCT_SSIM(uint8_t, float); else if (recon_t == ADCT_U8) ADCT_SSIM(uint8_t, uint8_t);
+    else ADCT_SSIM(uint8_t, int16_t);
+  } else {
+    if (recon_t == ADCT_F32) ADCT_SSIM(int16_t, float); else if (recon_t == ADCT_U8) ADCT_SSIM(int16_t, uint8_t);
+    else ADCT_SSIM(int16_t, int16_t);
+  }
+#undef ADCT_SSIM
+  count_launch();
+  if (adct_status e = launch_status()) return e;
+  const double nwin = (double)(g.height - 7) * (double)(g.width - 7);
+  launch_finalize_scaled(partial, tiles, g.n_images, 1.0 / nwin, ssim, st);
   return launch_status();
 }
 

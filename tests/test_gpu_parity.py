@@ -367,3 +367,38 @@ def test_roundtrip_blockmajor_tma_path(mats, name, out):
     else:
         rec = adct.approx_dct8x8_roundtrip(mats[name], xd, 10, torch.float32).cpu().numpy()
         assert rel_block_err(rec, _oracle_recon(name, x.numpy(), 10)) <= RTOL
+
+
+# --- SSIM (next row f1; reading A18) -------------------------------------------------------------
+
+from oracle import ssim as OS  # noqa: E402
+
+
+@pytest.mark.parametrize("shape", [(1, 8, 8), (2, 40, 56), (1, 72, 104), (2, 104, 264)])
+@pytest.mark.parametrize("rtype", [torch.float32, torch.uint8])
+def test_ssim_reduce_matches_oracle(shape, rtype):
+    n, h, w = shape
+    x = images("ar1", n, h, w, seed=h + w)
+    noise = torch.from_numpy(np.random.default_rng(h).normal(0, 12, size=(n, h, w)).astype(np.float32))
+    r = (x.float() + noise).clamp(-20, 280)
+    if rtype == torch.uint8:
+        r = r.clamp(0, 255).round().to(torch.uint8)
+    for clip in (adct.CLIP_NONE, adct.CLIP, adct.CLIP_ROUND):
+        got = adct.ssim_reduce(x.to(DEV), r.to(DEV), clip=clip).cpu().numpy()
+        ref = OS.ssim(x.numpy(), r.numpy(), clip=clip)
+        assert np.allclose(got, ref, rtol=1e-9, atol=1e-12), (got, ref)
+
+
+def test_ssim_identical_is_one_and_pipeline(mats):
+    """SSIM(x, x) = 1; and the C1-shaped pipeline fwd -> retain r -> inv (fused round trip) ->
+    SSIM against the oracle composition, for T1 and the DCT, at the paper's r = 3 and 14
+    (P:L2380-2444)."""
+    img = synth.ar1_field(1, 128, 128, 0.95, seed=1)
+    xd = img.to(DEV)
+    assert abs(float(adct.ssim_reduce(xd, xd)[0]) - 1.0) < 1e-12
+    for name in ("T1", "DCT"):
+        for r in (3, 14):
+            rec = adct.approx_dct8x8_roundtrip(mats[name], xd, r, torch.float32)
+            got = adct.ssim_reduce(xd, rec, clip=adct.CLIP).cpu().numpy()
+            ref = OS.ssim(img.numpy(), _oracle_recon(name, img.numpy(), r), clip=1)
+            assert np.allclose(got, ref, rtol=1e-6), (name, r, got, ref)
