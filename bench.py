@@ -253,6 +253,25 @@ def run_config(args):
                  f"in-place-sized out-of-place", name, ms, nblk, 256, "hbm", clk, cpu,
                  {"roundtrip_bit_exact": ok})
         del x, rec
+    if args.config in ("JAM", "all"):
+        # next row f2: 16- and 32-point JAM-scaled T1 (§6.2), fused round trip (r = N^2) of int16
+        # Laplace residual blocks (the C5 workload at HEVC block sizes), 2^26 8x8-equivalents
+        for n in (16, 32):
+            nb = (1 << 26) // ((n // 8) ** 2)
+            x = synth.laplace_blocks(nb * (n // 8) ** 2, seed=5, device=dev).reshape(nb, n, n)
+            rec = torch.empty_like(x)
+            ms, clk = _timed(lambda: adct.approx_dct_jam_roundtrip(n, x, n * n, torch.int16, recon=rec, stream=stream),
+                             args.steps, args.warmup, stream, dev)
+            ok = bool(torch.equal(rec, x))
+            from oracle import jam as OJ
+            xs = x[:256].cpu().numpy()
+            tt = OJ.T16 if n == 16 else OJ.T32
+            cpu = cpu_rate(lambda: OJ.recon_n(tt, xs, n * n), 256)
+            cpu["sample"] = f"256 blocks of {n}x{n}, by-definition forward + inverse"
+            emit(f"JAM{n} (next row f2): {nb} int16 Laplace(10) {n}x{n} blocks, fused T({n}) forward + inverse "
+                 f"(r={n * n}) -> int16; value = {n}x{n} blocks/s", f"T({n})", ms, nb, 4 * n * n, "hbm", clk, cpu,
+                 {"roundtrip_bit_exact": ok})
+            del x, rec
     if args.config in ("SSIM", "all"):
         # next row f1: fused round trip (fwd -> retain r=14 -> inv, fp32 recon) then SSIM with
         # 8x8 windows (reading A18) on the 512 luma frames of config 4
@@ -318,7 +337,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "SSIM", "all"],
+    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "SSIM", "JAM", "all"],
                     help="secondary BASELINE.json configuration instead of the config-4 headline")
     ap.add_argument("--c5-log2", type=int, default=26)
     args = ap.parse_args()

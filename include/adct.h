@@ -137,6 +137,16 @@ adct_status psnr_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
                         double peak, adct_clip clip, double* sse, double* psnr, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* 16- and 32-point transforms of §6.2: the Jridi-Alfalou-Meher scaling of
+ * T1 (Eq. 7; printed T(16), T(32) at P:L2669-2739, D(N) = diag(T T^T) at P:L2742-2770), as
+ * the round trip forward -> retention of the first r coefficients of the N x N zig-zag walk
+ * (reading A20) -> inverse C_hat^T B' C_hat, one pass, written as a reconstruction.
+ * n: 16 or 32.  src: device U8/I16 images with geometry g, H and W multiples of n, 16-byte
+ * aligned base and strides; recon: same geometry, dtype/clip policy as approx_dct8x8_roundtrip.
+ * r in 1..n^2.  The fp32 forward is exact for |samples| <= 7281. */
+adct_status approx_dct_jam_roundtrip(int32_t n, const void* src, adct_dtype src_t, adct_geom g, int32_t r,
+                                     void* recon, adct_dtype recon_t, adct_clip clip, void* stream);
+
 /* Structural similarity per image (citing Wang et al. 2004; the paper prints no
  * parameters — reading A18 in DESIGN.md, after SPEC S:L605): mean over every 8x8 window fully
  * inside the image (stride 1, uniform weights) of

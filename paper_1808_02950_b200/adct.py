@@ -28,7 +28,7 @@ SYMBOLS = [
     "adct_zigzag_order", "approx_dct8x8_fwd", "zonal_retain", "approx_dct8x8_inv", "psnr_reduce",
     "approx_dct8x8_fused_sse", "adct_host_workspace_bytes", "approx_dct8x8_fused_sse_host",
     "approx_dct8x8_fwd_quant", "adct_workspace_bytes", "adct_status_str", "adct_launch_count",
-    "approx_dct8x8_roundtrip", "ssim_reduce",
+    "approx_dct8x8_roundtrip", "ssim_reduce", "approx_dct_jam_roundtrip",
 ]
 
 
@@ -67,6 +67,7 @@ def _load() -> ctypes.CDLL:
     L.approx_dct8x8_fwd_quant.argtypes = [P, P, Geom, I32_, P, P]
     L.approx_dct8x8_roundtrip.argtypes = [P, P, S, Geom, I32_, P, S, S, P]
     L.ssim_reduce.argtypes = [P, S, P, S, Geom, D, S, P, P, ctypes.c_size_t, P]
+    L.approx_dct_jam_roundtrip.argtypes = [I32_, P, S, Geom, I32_, P, S, S, P]
     L.adct_workspace_bytes.argtypes = [Geom, I32_]
     L.adct_workspace_bytes.restype = ctypes.c_size_t
     L.adct_status_str.argtypes = [S]
@@ -243,6 +244,21 @@ def psnr_reduce(orig: torch.Tensor, recon: torch.Tensor, peak: float = 255.0, cl
                            int(clip), sse.data_ptr(), psnr.data_ptr(), workspace.data_ptr(), workspace.numel(),
                            _stream_ptr(stream)), "psnr_reduce")
     return sse, psnr
+
+
+def approx_dct_jam_roundtrip(n: int, src: torch.Tensor, r: int, recon_dtype=torch.float32, clip: int | None = None,
+                             recon: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """n x n (n = 16, 32) JAM-scaled T1 round trip of every block of src [N, H, W] (§6.2)."""
+    if clip is None:
+        clip = CLIP_ROUND if recon_dtype in (torch.int16, torch.uint8) else CLIP_NONE
+    g = geom_of(src)
+    if recon is None:
+        recon = torch.empty_strided(tuple(src.shape), src.stride(), dtype=recon_dtype, device=src.device)
+    if tuple(recon.stride()) != tuple(src.stride()):
+        raise ValueError("recon must have the strides of src")
+    _check(lib.approx_dct_jam_roundtrip(int(n), src.data_ptr(), dtype_code(src), g, int(r), recon.data_ptr(),
+                                        dtype_code(recon), int(clip), _stream_ptr(stream)), "approx_dct_jam_roundtrip")
+    return recon
 
 
 def ssim_reduce(orig: torch.Tensor, recon: torch.Tensor, peak: float = 255.0, clip: int = CLIP_NONE,

@@ -1,0 +1,282 @@
+// jam.cu — next row f2: 16- and 32-point transforms of §6.2, the
+// Jridi-Alfalou-Meher scaling of the paper's T1, through the round trip
+// forward -> zonal retention (N x N zig-zag, reading A20) -> inverse -> reconstruction.
+//
+// The N-point network is the JAM recursion itself (reading A19): u_i = x_i + x_{N-1-i},
+// v_i = x_i - x_{N-1-i}; rows 2k / 2k+1 of T(N) are row k of T(N/2) on u / v; the base is the
+// compile-time T1 network (24 adds + 6 shifts).  Its transpose (the inverse) runs the halves
+// first and the butterfly last.  All intermediates are integers < 2^24 for |x| <= 7281, so the
+// forward is exact in fp32.
+//
+// One CTA of 256 threads owns 256/N blocks.  Pass 1: thread (block b, row i) loads row i,
+// applies T(N) (row transform) and stores it to shared memory.  Pass 2: thread (b, column k)
+// applies T(N) down the column, the weights W_kl = keep_kl / (d_k d_l), d = diag(T T^T)
+// (P:L2742-2770), and T(N)^T back up the column.  Pass 3: thread (b, i) applies T(N)^T to its row
+// and writes the reconstruction.  An odd row pitch (N + 1) keeps the shared-memory passes
+// conflict-free.
+#include <cstring>
+#include <mutex>
+
+#include "adct_host.h"
+
+namespace adct {
+namespace {
+
+constexpr int kJamNT = 256;
+
+// y = T(N) x
+template <int N>
+struct Jam {
+  __device__ __forceinline__ static void fwd(const float* x, float* y) {
+    float u[N / 2], v[N / 2], yu[N / 2], yv[N / 2];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      u[i] = x[i] + x[N - 1 - i];
+      v[i] = x[i] - x[N - 1 - i];
+    }
+    Jam<N / 2>::fwd(u, yu);
+    Jam<N / 2>::fwd(v, yv);
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+      y[2 * k] = yu[k];
+      y[2 * k + 1] = yv[k];
+    }
+  }
+  // x = T(N)^T y
+  __device__ __forceinline__ static void inv(const float* y, float* x) {
+    float ye[N / 2], yo[N / 2], a[N / 2], b[N / 2];
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+      ye[k] = y[2 * k];
+      yo[k] = y[2 * k + 1];
+    }
+    Jam<N / 2>::inv(ye, a);
+    Jam<N / 2>::inv(yo, b);
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      x[i] = a[i] + b[i];
+      x[N - 1 - i] = a[i] - b[i];
+    }
+  }
+};
+
+__device__ DevMat g_jam_unused;  // T1Mat ignores its DevMat: the network is compile-time
+
+template <>
+struct Jam<8> {
+  __device__ __forceinline__ static void fwd(const float* x, float* y) { fwd8(T1Mat(g_jam_unused), x, y); }
+  __device__ __forceinline__ static void inv(const float* y, float* x) {
+    inv8<T1Mat, 0xffu>(T1Mat(g_jam_unused), y, x);
+  }
+};
+
+template <int N>
+struct JamW {
+  float w[N * N];  // keep_kl / (d_k d_l)
+};
+
+// N samples of one row as fp32 (16-byte vector loads; rows are 16-byte aligned)
+template <int N>
+__device__ __forceinline__ void load_row(const uint8_t* p, float* x) {
+#pragma unroll
+  for (int c = 0; c < N / 16; ++c) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + c);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x[c * 16 + q] = (float)((w[q >> 2] >> (8 * (q & 3))) & 0xffu);
+  }
+}
+template <int N>
+__device__ __forceinline__ void load_row(const int16_t* p, float* x) {
+#pragma unroll
+  for (int c = 0; c < N / 8; ++c) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + c);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[c * 8 + q] = (float)(int16_t)((w[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void store_row_any(void* recon, int64_t off, int out_t, const float* x) {
+  if (out_t == ADCT_F32) {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(recon) + off);
+#pragma unroll
+    for (int c = 0; c < N / 4; ++c) o[c] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+  } else if (out_t == ADCT_I16) {
+    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<int16_t*>(recon) + off);
+#pragma unroll
+    for (int c = 0; c < N / 8; ++c) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = (uint32_t)(uint16_t)(int16_t)x[8 * c + 2 * q] | ((uint32_t)(uint16_t)(int16_t)x[8 * c + 2 * q + 1] << 16);
+      o[c] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  } else {
+    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(recon) + off);
+#pragma unroll
+    for (int c = 0; c < N / 16; ++c) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = (uint32_t)(uint8_t)x[16 * c + 4 * q] | ((uint32_t)(uint8_t)x[16 * c + 4 * q + 1] << 8) |
+               ((uint32_t)(uint8_t)x[16 * c + 4 * q + 2] << 16) | ((uint32_t)(uint8_t)x[16 * c + 4 * q + 3] << 24);
+      o[c] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+template <int N, typename SrcT>
+__global__ void __launch_bounds__(kJamNT) jam_roundtrip_kernel(const SrcT* __restrict__ src, KGeom g, JamW<N> wt,
+                                                               uint32_t nblocks, FastDiv dnbi, FastDiv dbw,
+                                                               int out_t, int clip, float lo, float hi,
+                                                               void* __restrict__ recon) {
+  constexpr int BPC = kJamNT / N;  // blocks per CTA
+  constexpr int P = N + 1;         // odd row pitch: row writes and column reads are conflict-free
+  __shared__ float sm[BPC * N * P];
+  __shared__ float sw[N * N];  // weights: lanes read different columns (a constant-bank read would serialise)
+  for (int t = threadIdx.x; t < N * N; t += kJamNT) sw[t] = wt.w[t];
+  __syncthreads();
+  const int bl = threadIdx.x / N, i = threadIdx.x % N;  // thread = (block, row i) = (block, column i)
+  for (uint32_t b0 = blockIdx.x * BPC; b0 < nblocks; b0 += gridDim.x * BPC) {
+    const uint32_t b = b0 + bl;
+    const bool valid = b < nblocks;
+    int64_t off = 0;
+    if (valid) {
+      const uint32_t img = fdiv(b, dnbi);
+      const uint32_t q = b - img * g.nbi;
+      const uint32_t by = fdiv(q, dbw);
+      const uint32_t bx = q - by * g.bw;
+      off = (int64_t)img * g.image_stride + ((int64_t)by * N + i) * g.row_stride + (int64_t)bx * N;
+    }
+    float* row = sm + (bl * N + i) * P;
+    {  // pass 1: row i of block bl, forward
+      float x[N], y[N];
+      if (valid) load_row<N>(src + off, x);
+      else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = 0.0f;
+      }
+      Jam<N>::fwd(x, y);
+#pragma unroll
+      for (int j = 0; j < N; ++j) row[j] = y[j];
+    }
+    __syncthreads();
+    {  // pass 2: column i (frequency l = i) of block bl: forward, weights, inverse
+      float c[N], y[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) c[k] = sm[(bl * N + k) * P + i];
+      Jam<N>::fwd(c, y);
+#pragma unroll
+      for (int k = 0; k < N; ++k) y[k] *= sw[k * N + i];
+      Jam<N>::inv(y, c);
+#pragma unroll
+      for (int k = 0; k < N; ++k) sm[(bl * N + k) * P + i] = c[k];
+    }
+    __syncthreads();
+    {  // pass 3: row i, inverse, store
+      float z[N], x[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) z[j] = row[j];
+      Jam<N>::inv(z, x);
+      if (valid) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          float v = x[j];
+          if (clip != ADCT_CLIP_NONE) v = fminf(fmaxf(v, lo), hi);
+          if (clip == ADCT_CLIP_ROUND) v = rintf(v);
+          x[j] = v;
+        }
+        store_row_any<N>(recon, off, out_t, x);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// n x n zig-zag walk (reading A20): anti-diagonals d = k + l in order, even ones bottom-left
+// to top-right
+template <int N>
+void zigzag_keep(int r, bool* keep) {
+  int z = 0;
+  for (int d = 0; d < 2 * N - 1; ++d) {
+    int ks[2 * N];
+    int c = 0;
+    for (int k = 0; k < N; ++k)
+      if (d - k >= 0 && d - k < N) ks[c++] = k;
+    for (int t = 0; t < c; ++t) {
+      const int k = (d % 2 == 0) ? ks[c - 1 - t] : ks[t];
+      keep[k * N + (d - k)] = z < r;
+      ++z;
+    }
+  }
+}
+
+template <int N, typename SrcT>
+adct_status launch_jam(const void* src, const adct_geom& g, int32_t r, void* recon, adct_dtype recon_t,
+                       adct_clip clip, float lo, float hi, cudaStream_t st) {
+  // d = diag(T(N) T(N)^T): D(16) = 4 (I2 x diag(4,9,10,9) x I2), D(32) = 2 D(16) x I2
+  double d8[8] = {8, 18, 20, 18, 8, 18, 20, 18};
+  double d[N];
+  for (int k = 0; k < N; ++k) d[k] = d8[k / (N / 8)] * (double)(N / 8);
+  bool keep[N * N];
+  zigzag_keep<N>(r, keep);
+  JamW<N> wt;
+  for (int k = 0; k < N; ++k)
+    for (int l = 0; l < N; ++l) wt.w[k * N + l] = keep[k * N + l] ? (float)(1.0 / (d[k] * d[l])) : 0.0f;
+  KGeom kg;
+  kg.image_stride = g.image_stride;
+  kg.row_stride = g.row_stride;
+  kg.bw = (uint32_t)(g.width / N);
+  kg.bh = (uint32_t)(g.height / N);
+  kg.nbi = kg.bw * kg.bh;
+  kg.n_images = (uint32_t)g.n_images;
+  const uint32_t nb = (uint32_t)(g.n_images * kg.nbi);
+  if (nb == 0) return ADCT_OK;
+  constexpr int BPC = kJamNT / N;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t need = ((int64_t)nb + BPC - 1) / BPC, cap = (int64_t)sms * 8;
+  const unsigned grid = (unsigned)(need < cap ? need : cap);
+  jam_roundtrip_kernel<N, SrcT><<<grid, kJamNT, 0, st>>>((const SrcT*)src, kg, wt, nb, make_fastdiv(kg.nbi),
+                                                         make_fastdiv(kg.bw), (int)recon_t, (int)clip, lo, hi, recon);
+  count_launch();
+  return launch_status();
+}
+
+}  // namespace
+}  // namespace adct
+
+using namespace adct;
+
+extern "C" adct_status approx_dct_jam_roundtrip(int32_t n, const void* src, adct_dtype src_t, adct_geom g, int32_t r,
+                                               void* recon, adct_dtype recon_t, adct_clip clip, void* stream) {
+  if (!src || !recon) return ADCT_E_INVALID_ARGUMENT;
+  if (n != 16 && n != 32) return ADCT_E_INVALID_ARGUMENT;
+  if (g.n_images < 0 || g.height <= 0 || g.width <= 0 || g.height % n || g.width % n) return ADCT_E_INVALID_ARGUMENT;
+  if (g.row_stride < g.width || (g.n_images > 1 && g.image_stride < (int64_t)g.height * g.row_stride))
+    return ADCT_E_INVALID_ARGUMENT;
+  if (g.n_images * (int64_t)(g.height / n) * (g.width / n) >= ((int64_t)1 << 31)) return ADCT_E_INVALID_ARGUMENT;
+  if (src_t != ADCT_U8 && src_t != ADCT_I16) return ADCT_E_INVALID_ARGUMENT;
+  if (r < 1 || r > n * n) return ADCT_E_INVALID_ARGUMENT;
+  if (clip != ADCT_CLIP_NONE && clip != ADCT_CLIP && clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  if (recon_t == ADCT_U8 || recon_t == ADCT_I16) {
+    if (clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  } else if (recon_t != ADCT_F32) {
+    return ADCT_E_INVALID_ARGUMENT;
+  }
+  const int esz = src_t == ADCT_U8 ? 1 : 2, osz = recon_t == ADCT_F32 ? 4 : (recon_t == ADCT_I16 ? 2 : 1);
+  // 16-byte vector rows: aligned bases and strides (in both element sizes)
+  if ((uintptr_t)src % 16 || (uintptr_t)recon % 16 || (g.row_stride * esz) % 16 || (g.row_stride * osz) % 16 ||
+      (g.n_images > 1 && ((g.image_stride * esz) % 16 || (g.image_stride * osz) % 16)))
+    return ADCT_E_ALIGNMENT;
+  const float lo = src_t == ADCT_U8 ? 0.0f : -32768.0f, hi = src_t == ADCT_U8 ? 255.0f : 32767.0f;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 16)
+    return src_t == ADCT_U8 ? launch_jam<16, uint8_t>(src, g, r, recon, recon_t, clip, lo, hi, st)
+                            : launch_jam<16, int16_t>(src, g, r, recon, recon_t, clip, lo, hi, st);
+  return src_t == ADCT_U8 ? launch_jam<32, uint8_t>(src, g, r, recon, recon_t, clip, lo, hi, st)
+                          : launch_jam<32, int16_t>(src, g, r, recon, recon_t, clip, lo, hi, st);
+}

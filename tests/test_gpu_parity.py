@@ -402,3 +402,50 @@ def test_ssim_identical_is_one_and_pipeline(mats):
             got = adct.ssim_reduce(xd, rec, clip=adct.CLIP).cpu().numpy()
             ref = OS.ssim(img.numpy(), _oracle_recon(name, img.numpy(), r), clip=1)
             assert np.allclose(got, ref, rtol=1e-6), (name, r, got, ref)
+
+
+# --- 16/32-point JAM transforms (next row f2; readings A19, A20) ---------------------------------
+
+from oracle import jam as OJ  # noqa: E402
+
+
+def _rel_err_nn(got, ref, n):
+    g = OJ.blocks_n(got, n).reshape(-1, n * n).astype(np.float64)
+    o = OJ.blocks_n(ref, n).reshape(-1, n * n).astype(np.float64)
+    return float(np.max(np.abs(g - o).max(axis=1) / np.maximum(np.abs(o).max(axis=1), 1.0)))
+
+
+@pytest.mark.parametrize("n", [16, 32])
+@pytest.mark.parametrize("kind", ["ar1", "laplace"])
+def test_jam_roundtrip_f32_matches_oracle(n, kind):
+    t = OJ.T16 if n == 16 else OJ.T32
+    img = images(kind, 2, 2 * n, 3 * n, seed=n)
+    for r in (1, 3, 10, n * n // 3, n * n):
+        rec = adct.approx_dct_jam_roundtrip(n, img.to(DEV), r, torch.float32).cpu().numpy()
+        ref = OJ.recon_n(t, img.numpy(), r)
+        assert _rel_err_nn(rec, ref, n) <= RTOL, (n, r)
+
+
+@pytest.mark.parametrize("n", [16, 32])
+def test_jam_roundtrip_int16_bit_exact_and_u8(n):
+    nb = 4096 + 3
+    x = synth.laplace_blocks(nb * (n // 8) ** 2, seed=n).reshape(nb, n, n)   # n x n residual blocks
+    rec = adct.approx_dct_jam_roundtrip(n, x.to(DEV), n * n, torch.int16)
+    assert torch.equal(rec.cpu(), x)
+    img = images("ar1", 1, 4 * n, 5 * n, seed=3)
+    rec8 = adct.approx_dct_jam_roundtrip(n, img.to(DEV), 10, torch.uint8).cpu().numpy()
+    ref = OJ.recon_n(OJ.T16 if n == 16 else OJ.T32, img.numpy(), 10)
+    ref_u8 = np.clip(np.rint(ref), 0, 255)
+    diff = np.abs(rec8.astype(np.int64) - ref_u8)
+    assert diff.max() <= 1
+    assert np.all(np.abs(np.abs(ref - np.floor(ref)) - 0.5)[diff > 0] < 1e-3)
+
+
+def test_jam_argument_errors():
+    x = torch.zeros((1, 16, 16), dtype=torch.int16, device=DEV)
+    with pytest.raises(adct.AdctError):
+        adct.approx_dct_jam_roundtrip(8, x, 1, torch.float32)
+    with pytest.raises(adct.AdctError):
+        adct.approx_dct_jam_roundtrip(16, x, 257, torch.float32)
+    with pytest.raises(adct.AdctError):
+        adct.approx_dct_jam_roundtrip(32, x, 1, torch.float32)  # 16 x 16 image, 32-point blocks
