@@ -253,6 +253,40 @@ def run_config(args):
                  f"in-place-sized out-of-place", name, ms, nblk, 256, "hbm", clk, cpu,
                  {"roundtrip_bit_exact": ok})
         del x, rec
+    if args.config in ("GREEDY", "all"):
+        # next row f3: the greedy angle search of §3 (Fig. 2) — D2 = {0,+-1,+-2}^8 with rows 1, 5
+        # fixed over all 720 orders (§4.1), and D1 = {0,+-1}^8 over all 8! = 40320 orders (§3.4)
+        import itertools
+        from oracle import greedy as OG
+        from oracle import matrices as OMM
+        for name, ent, fixed, orders in (
+                ("D2, rows 1,5 fixed, 720 orders", OG.P2, OG.FIXED_ROWS,
+                 np.array(list(itertools.permutations([1, 2, 3, 5, 6, 7])), dtype=np.int32)),
+                ("D1, all 40320 orders", OG.P1, None, np.array(list(itertools.permutations(range(8))), dtype=np.int32))):
+            wsg = torch.empty(adct.lib.adct_greedy_workspace_bytes(len(ent)), dtype=torch.uint8, device=dev)
+            ms, clk = _timed(lambda: adct.greedy_search(OMM.C, ent, orders, fixed=fixed, device=dev, workspace=wsg,
+                                                        stream=stream), args.steps, args.warmup, stream, dev)
+            mats, status = adct.greedy_search(OMM.C, ent, orders, fixed=fixed, device=dev, workspace=wsg)
+            st = status.cpu().numpy()
+            distinct = len({m.tobytes() for m, s_ in zip(mats.cpu().numpy(), st) if s_ == 0})
+            srch = OG.Search(ent)
+            t0 = time.perf_counter()
+            nsmp = 720 if fixed else 200
+            for o in orders[:nsmp]:
+                srch.solve(tuple(o), fixed)
+            cdt = time.perf_counter() - t0
+            cand = len(orders) * (8 - len(fixed or {})) * len(ent) ** 8
+            line = {"metric": "greedy search: candidate evaluations/s", "value": cand / (ms * 1e-3),
+                    "unit": "candidates/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                    "higher_is_better": True, "dtype": "f64 score / int8 dp4a orthogonality", "data": "exact DCT C",
+                    "config": {"workload": f"GREEDY (next row f3): {name}", "feasible": int((st == 0).sum()),
+                               "infeasible": int((st == 1).sum()), "distinct_matrices": distinct},
+                    "roofline": {"bound": "alu", "note": "candidate scan: DP4A orthogonality + fp64 score loads"},
+                    "clocks": clk,
+                    "cpu_baseline": {"value": nsmp * (8 - len(fixed or {})) * len(ent) ** 8 / cdt,
+                                     "unit": "candidates/s", "cores": 1, "kind": "oracle",
+                                     "sample": f"{nsmp} orders, numpy oracle (memoised orthogonality masks)"}}
+            print(json.dumps(line), flush=True)
     if args.config in ("JAM", "all"):
         # next row f2: 16- and 32-point JAM-scaled T1 (§6.2), fused round trip (r = N^2) of int16
         # Laplace residual blocks (the C5 workload at HEVC block sizes), 2^26 8x8-equivalents
@@ -337,7 +371,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "SSIM", "JAM", "all"],
+    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "SSIM", "JAM", "GREEDY", "all"],
                     help="secondary BASELINE.json configuration instead of the config-4 headline")
     ap.add_argument("--c5-log2", type=int, default=26)
     args = ap.parse_args()

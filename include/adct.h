@@ -147,6 +147,26 @@ adct_status psnr_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
 adct_status approx_dct_jam_roundtrip(int32_t n, const void* src, adct_dtype src_t, adct_geom g, int32_t r,
                                      void* recon, adct_dtype recon_t, adct_clip clip, void* stream);
 
+/* The greedy angle search of §3 (Eq. 5-6; Fig. 2) that produces T1
+ * and T2 (§4.1), one permutation sequence per CTA.  For each sequence the free
+ * rows are placed in the given order; row k is the vector of D = P^8 with the largest
+ * s(d) = <c_k, d> / (|d| |c_k|) (fp64, reading A21: smallest angle) among the non-zero
+ * vectors orthogonal to every placed row (A23), ties to the earliest vector of the
+ * lexicographic enumeration with the entries in ascending order (A22).
+ * c: HOST fp64 [64], rows of the matrix to approximate (the orthonormal DCT, reading A1).
+ * entries: HOST int32 [n_entries] (1..8 distinct values in [-127, 127]; sorted internally).
+ * fixed / fixed_mask: HOST rows pre-assigned before the search (bit k of the mask: row k taken
+ * from fixed[8k..8k+7]; §4.1 fixes rows 0 and 4).  orders: DEVICE int32
+ * [n_orders][8 - popcount(fixed_mask)], the free row indices in placement order.
+ * out: DEVICE int32 [n_orders][64] (zero for infeasible sequences); status: DEVICE int32
+ * [n_orders], 0 = ok, 1 = no orthogonal candidate left at some step (A24), 2 = invalid
+ * sequence (an index outside 0..7, a fixed row, or a repeated row).
+ * workspace >= adct_greedy_workspace_bytes(n_entries) (the packed space and the scores). */
+size_t adct_greedy_workspace_bytes(int32_t n_entries);
+adct_status adct_greedy_search(const double c[64], const int32_t* entries, int32_t n_entries, const int32_t fixed[64],
+                               uint32_t fixed_mask, const int32_t* orders, int32_t n_orders, int32_t* out,
+                               int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Structural similarity per image (citing Wang et al. 2004; the paper prints no
  * parameters — reading A18 in DESIGN.md, after SPEC S:L605): mean over every 8x8 window fully
  * inside the image (stride 1, uniform weights) of

@@ -28,7 +28,8 @@ SYMBOLS = [
     "adct_zigzag_order", "approx_dct8x8_fwd", "zonal_retain", "approx_dct8x8_inv", "psnr_reduce",
     "approx_dct8x8_fused_sse", "adct_host_workspace_bytes", "approx_dct8x8_fused_sse_host",
     "approx_dct8x8_fwd_quant", "adct_workspace_bytes", "adct_status_str", "adct_launch_count",
-    "approx_dct8x8_roundtrip", "ssim_reduce", "approx_dct_jam_roundtrip",
+    "approx_dct8x8_roundtrip", "ssim_reduce", "approx_dct_jam_roundtrip", "adct_greedy_workspace_bytes",
+    "adct_greedy_search",
 ]
 
 
@@ -68,6 +69,9 @@ def _load() -> ctypes.CDLL:
     L.approx_dct8x8_roundtrip.argtypes = [P, P, S, Geom, I32_, P, S, S, P]
     L.ssim_reduce.argtypes = [P, S, P, S, Geom, D, S, P, P, ctypes.c_size_t, P]
     L.approx_dct_jam_roundtrip.argtypes = [I32_, P, S, Geom, I32_, P, S, S, P]
+    L.adct_greedy_workspace_bytes.argtypes = [I32_]
+    L.adct_greedy_workspace_bytes.restype = ctypes.c_size_t
+    L.adct_greedy_search.argtypes = [P, P, I32_, P, ctypes.c_uint32, P, I32_, P, P, P, ctypes.c_size_t, P]
     L.adct_workspace_bytes.argtypes = [Geom, I32_]
     L.adct_workspace_bytes.restype = ctypes.c_size_t
     L.adct_status_str.argtypes = [S]
@@ -77,7 +81,7 @@ def _load() -> ctypes.CDLL:
     for name in SYMBOLS:
         fn = getattr(L, name)
         if name not in ("adct_matrix_destroy", "adct_host_workspace_bytes", "adct_workspace_bytes",
-                        "adct_status_str", "adct_launch_count"):
+                        "adct_status_str", "adct_launch_count", "adct_greedy_workspace_bytes"):
             fn.restype = S
     return L
 
@@ -259,6 +263,31 @@ def approx_dct_jam_roundtrip(n: int, src: torch.Tensor, r: int, recon_dtype=torc
     _check(lib.approx_dct_jam_roundtrip(int(n), src.data_ptr(), dtype_code(src), g, int(r), recon.data_ptr(),
                                         dtype_code(recon), int(clip), _stream_ptr(stream)), "approx_dct_jam_roundtrip")
     return recon
+
+
+def greedy_search(c, entries, orders, fixed: dict | None = None, device=None, workspace=None, stream=None):
+    """Greedy angle search (§3, Fig. 2) for every sequence in `orders` ([n, n_free] row indices):
+    returns (matrices int32 [n, 8, 8], status int32 [n]) on `device`."""
+    import numpy as _np
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    c64 = _np.ascontiguousarray(_np.asarray(c, dtype=_np.float64).reshape(64))
+    ent = _np.ascontiguousarray(_np.asarray(entries, dtype=_np.int32))
+    fx = _np.zeros(64, dtype=_np.int32)
+    mask = 0
+    for k, row in (fixed or {}).items():
+        fx[8 * k:8 * k + 8] = row
+        mask |= 1 << int(k)
+    od = torch.as_tensor(_np.ascontiguousarray(_np.asarray(orders, dtype=_np.int32)), device=dev)
+    n = od.shape[0]
+    out = torch.empty((n, 8, 8), dtype=torch.int32, device=dev)
+    status = torch.empty(n, dtype=torch.int32, device=dev)
+    nbytes = lib.adct_greedy_workspace_bytes(len(ent))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    _check(lib.adct_greedy_search(c64.ctypes.data, ent.ctypes.data, len(ent), fx.ctypes.data, mask, od.data_ptr(), n,
+                                  out.data_ptr(), status.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                  _stream_ptr(stream)), "adct_greedy_search")
+    return out, status
 
 
 def ssim_reduce(orig: torch.Tensor, recon: torch.Tensor, peak: float = 255.0, clip: int = CLIP_NONE,

@@ -449,3 +449,56 @@ def test_jam_argument_errors():
         adct.approx_dct_jam_roundtrip(16, x, 257, torch.float32)
     with pytest.raises(adct.AdctError):
         adct.approx_dct_jam_roundtrip(32, x, 1, torch.float32)  # 16 x 16 image, 32-point blocks
+
+
+# --- greedy angle search (next row f3; readings A21-A24) -----------------------------------------
+
+from oracle import greedy as OG  # noqa: E402
+import itertools as _it  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def greedy_spaces():
+    return {1: OG.Search(OG.P1), 2: OG.Search(OG.P2)}
+
+
+@pytest.mark.parametrize("space", [1, 2])
+def test_greedy_search_fixed_rows_all_orders(greedy_spaces, space):
+    """§4.1 setting: rows 1 and 5 fixed, all 720 orders of the other six; every sequence's
+    matrix (or infeasibility) equals the oracle's; D2 yields exactly T1 and T2."""
+    s = greedy_spaces[space]
+    ref = s.derive_all()
+    orders = np.array([o for o, _ in ref], dtype=np.int32)
+    mats, status = adct.greedy_search(M.C, OG.P1 if space == 1 else OG.P2, orders, fixed=OG.FIXED_ROWS, device=DEV)
+    mats, status = mats.cpu().numpy(), status.cpu().numpy()
+    for n, (o, m) in enumerate(ref):
+        if m is None:
+            assert status[n] == 1, o
+        else:
+            assert status[n] == 0 and np.array_equal(mats[n], m), o
+    if space == 2:
+        got = {mats[n].tobytes() for n in range(len(ref)) if status[n] == 0}
+        assert got == {np.array(M.T1, dtype=np.int32).tobytes(), np.array(M.T2, dtype=np.int32).tobytes()}
+
+
+def test_greedy_search_free_orders_d1(greedy_spaces):
+    """All eight rows free (§3.4): the worked forward/reverse orders and 62 sampled
+    permutations of 8! over D1, against the oracle."""
+    s = greedy_spaces[1]
+    rng = np.random.default_rng(7)
+    perms = [tuple(range(8)), tuple(range(7, -1, -1))] + [tuple(rng.permutation(8)) for _ in range(62)]
+    mats, status = adct.greedy_search(M.C, OG.P1, np.array(perms, dtype=np.int32), device=DEV)
+    mats, status = mats.cpu().numpy(), status.cpu().numpy()
+    for n, p in enumerate(perms):
+        m = s.solve(p)
+        if m is None:
+            assert status[n] == 1
+        else:
+            assert status[n] == 0 and np.array_equal(mats[n], m), p
+
+
+def test_greedy_search_invalid_sequences():
+    mats, status = adct.greedy_search(M.C, OG.P1, np.array([[1, 2, 3, 5, 6, 9], [1, 1, 2, 3, 5, 6],
+                                                            [0, 1, 2, 3, 5, 6]], dtype=np.int32),
+                                      fixed=OG.FIXED_ROWS, device=DEV)
+    assert status.cpu().tolist() == [2, 2, 2]
