@@ -253,6 +253,32 @@ def run_config(args):
                  f"in-place-sized out-of-place", name, ms, nblk, 256, "hbm", clk, cpu,
                  {"roundtrip_bit_exact": ok})
         del x, rec
+    if args.config in ("MERIT", "all"):
+        # next row f4: Table 4 figures of merit of the nine matrices over 4096 values of rho in
+        # (0, 1) — the Fig. 1 coding-gain curves
+        from oracle import merit as OMR
+        names = catalog.CONFIG2_ORDER
+        mats = [adct.Matrix.from_real(catalog.exact_dct(), "DCT") if nm == "DCT" else
+                adct.Matrix.from_int(catalog.INTEGER[nm], nm) for nm in names]
+        rho = torch.linspace(0.0005, 0.9995, 4096, dtype=torch.float64, device=dev)
+        ms, clk = _timed(lambda: adct.merit_batch(mats, rho, stream=stream), args.steps, args.warmup, stream, dev)
+        out = adct.merit_batch(mats, rho).cpu().numpy()
+        t1, dct = names.index("T1"), names.index("DCT")
+        t0 = time.perf_counter()
+        chat = OMR.M.c_hat(np.array(catalog.T1).reshape(8, 8))
+        for r in rho.cpu().numpy()[:256]:
+            OMR.unified_coding_gain(chat, float(r))
+        cdt = (time.perf_counter() - t0) / 256
+        line = {"metric": "figure-of-merit evaluations/s (4 measures per (matrix, rho))",
+                "value": len(names) * 4096 / (ms * 1e-3), "unit": "(matrix, rho)/s", "n_gpus": 1, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f64",
+                "data": "the nine matrices of C2", "config": {"workload": "MERIT (next row f4): Table 4 measures of 9 "
+                                                              "matrices x 4096 rho (Fig. 1 curves)"},
+                "roofline": {"bound": "alu", "note": "fp64 8x8 products per thread; launch-latency sized"},
+                "clocks": clk, "fig1_max_cg_gap_T1_minus_DCT_dB": float((out[t1, :, 2] - out[dct, :, 2]).max()),
+                "cpu_baseline": {"value": 1.0 / cdt, "unit": "(matrix, rho)/s", "cores": 1, "kind": "oracle",
+                                 "sample": "256 rho values, C*_g of T1 only (numpy oracle)"}}
+        print(json.dumps(line), flush=True)
     if args.config in ("GREEDY", "all"):
         # next row f3: the greedy angle search of §3 (Fig. 2) — D2 = {0,+-1,+-2}^8 with rows 1, 5
         # fixed over all 720 orders (§4.1), and D1 = {0,+-1}^8 over all 8! = 40320 orders (§3.4)
@@ -371,7 +397,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "SSIM", "JAM", "GREEDY", "all"],
+    ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "SSIM", "JAM", "GREEDY", "MERIT", "all"],
                     help="secondary BASELINE.json configuration instead of the config-4 headline")
     ap.add_argument("--c5-log2", type=int, default=26)
     args = ap.parse_args()

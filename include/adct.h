@@ -98,6 +98,9 @@ adct_status adct_matrix_info(const adct_matrix* m, double s[8], double g[64], in
 
 void adct_matrix_destroy(adct_matrix* m);
 
+/* C_hat = S T (integer matrices) or the real matrix itself, row-major fp64 (host). */
+adct_status adct_matrix_chat(const adct_matrix* m, double chat[64]);
+
 /* The zig-zag order the device path uses: order[z] = raster index (k*8+l) of the z-th
  * coefficient.  Host-only. */
 adct_status adct_zigzag_order(int32_t order[64]);
@@ -166,6 +169,16 @@ size_t adct_greedy_workspace_bytes(int32_t n_entries);
 adct_status adct_greedy_search(const double c[64], const int32_t* entries, int32_t n_entries, const int32_t fixed[64],
                                uint32_t fixed_mask, const int32_t* orders, int32_t n_orders, int32_t* out,
                                int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Matrix figures of merit of §4.2 for every (matrix, rho) pair: Table 4's
+ * total error energy eps = pi ||C - C_hat||_F^2, MSE = tr((C - C_hat) R_x (C - C_hat)^T)/8,
+ * unified coding gain C*_g (B_i from the rows of C_hat^{-1}, reading A3) and transform
+ * efficiency eta, with (R_x)_ij = rho^|i-j| — the Fig. 1 curves are C*_g
+ * against rho.  c: HOST fp64 [64] exact DCT (reading A1); chat, ginv: DEVICE fp64 [n][64]
+ * (C_hat = S T and its inverse, row-major); rho: DEVICE fp64 [m]; out: DEVICE fp64
+ * [n][m][4] = (eps, MSE, C*_g in dB, eta in %). */
+adct_status adct_merit_batch(const double c[64], const double* chat, const double* ginv, int32_t n,
+                             const double* rho, int32_t m, double* out, void* stream);
 
 /* Structural similarity per image (citing Wang et al. 2004; the paper prints no
  * parameters — reading A18 in DESIGN.md, after SPEC S:L605): mean over every 8x8 window fully

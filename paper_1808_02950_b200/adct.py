@@ -29,7 +29,7 @@ SYMBOLS = [
     "approx_dct8x8_fused_sse", "adct_host_workspace_bytes", "approx_dct8x8_fused_sse_host",
     "approx_dct8x8_fwd_quant", "adct_workspace_bytes", "adct_status_str", "adct_launch_count",
     "approx_dct8x8_roundtrip", "ssim_reduce", "approx_dct_jam_roundtrip", "adct_greedy_workspace_bytes",
-    "adct_greedy_search",
+    "adct_greedy_search", "adct_merit_batch", "adct_matrix_chat",
 ]
 
 
@@ -71,6 +71,8 @@ def _load() -> ctypes.CDLL:
     L.approx_dct_jam_roundtrip.argtypes = [I32_, P, S, Geom, I32_, P, S, S, P]
     L.adct_greedy_workspace_bytes.argtypes = [I32_]
     L.adct_greedy_workspace_bytes.restype = ctypes.c_size_t
+    L.adct_merit_batch.argtypes = [P, P, P, I32_, P, I32_, P, P]
+    L.adct_matrix_chat.argtypes = [P, P]
     L.adct_greedy_search.argtypes = [P, P, I32_, P, ctypes.c_uint32, P, I32_, P, P, P, ctypes.c_size_t, P]
     L.adct_workspace_bytes.argtypes = [Geom, I32_]
     L.adct_workspace_bytes.restype = ctypes.c_size_t
@@ -172,6 +174,11 @@ class Matrix:
                                     ctypes.byref(ro), ctypes.byref(ii), ctypes.byref(mu), ctypes.byref(mi),
                                     ctypes.byref(sp)), "adct_matrix_info")
         return MatrixInfo(list(s), list(g), bool(ro.value), bool(ii.value), mu.value, mi.value, bool(sp.value))
+
+    def chat(self) -> list:
+        c = (ctypes.c_double * 64)()
+        _check(lib.adct_matrix_chat(self.handle, ctypes.cast(c, ctypes.c_void_p)), "adct_matrix_chat")
+        return list(c)
 
     def close(self) -> None:
         if self._h:
@@ -288,6 +295,23 @@ def greedy_search(c, entries, orders, fixed: dict | None = None, device=None, wo
                                   out.data_ptr(), status.data_ptr(), workspace.data_ptr(), workspace.numel(),
                                   _stream_ptr(stream)), "adct_greedy_search")
     return out, status
+
+
+def merit_batch(mats: list, rho: torch.Tensor, c_exact=None, stream=None) -> torch.Tensor:
+    """Figures of merit (eps, MSE, C*_g, eta) of §4.2 for every (descriptor, rho): C_hat and its
+    inverse come from the descriptors (adct_matrix_chat, adct_matrix_info's G); rho fp64 [m] on
+    the device; returns fp64 [n, m, 4]."""
+    import numpy as _np
+    from . import catalog as _cat
+    c = _np.ascontiguousarray(_np.asarray(c_exact if c_exact is not None else _cat.exact_dct(), dtype=_np.float64))
+    dev = rho.device
+    chat = torch.tensor([m.chat() for m in mats], dtype=torch.float64, device=dev)
+    ginv = torch.tensor([m.info().g for m in mats], dtype=torch.float64, device=dev)
+    rho = rho.contiguous().to(torch.float64)
+    out = torch.empty((chat.shape[0], rho.numel(), 4), dtype=torch.float64, device=chat.device)
+    _check(lib.adct_merit_batch(c.ctypes.data, chat.data_ptr(), ginv.data_ptr(), chat.shape[0], rho.data_ptr(),
+                                rho.numel(), out.data_ptr(), _stream_ptr(stream)), "adct_merit_batch")
+    return out
 
 
 def ssim_reduce(orig: torch.Tensor, recon: torch.Tensor, peak: float = 255.0, clip: int = CLIP_NONE,

@@ -277,6 +277,12 @@ const char* adct_status_str(adct_status s) {
 
 int64_t adct_launch_count(void) { return g_launches.load(); }
 
+adct_status adct_matrix_chat(const adct_matrix* m, double chat[64]) {
+  if (!m || !chat) return ADCT_E_INVALID_ARGUMENT;
+  for (int i = 0; i < 64; ++i) chat[i] = m->chat[i];
+  return ADCT_OK;
+}
+
 size_t adct_workspace_bytes(adct_geom g, int32_t n_r) {
   (void)n_r;  // per-image partials hold all 64 r slots of the sweep kernel
   const int64_t a = (fused_chunks(g) > sweep_chunks(g) ? fused_chunks(g) : sweep_chunks(g)) * 64;

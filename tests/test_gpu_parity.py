@@ -502,3 +502,24 @@ def test_greedy_search_invalid_sequences():
                                                             [0, 1, 2, 3, 5, 6]], dtype=np.int32),
                                       fixed=OG.FIXED_ROWS, device=DEV)
     assert status.cpu().tolist() == [2, 2, 2]
+
+
+# --- figures of merit (next row f4) ----------------------------------------------------------------
+
+from oracle import merit as OMR  # noqa: E402
+
+
+def test_merit_batch_matches_oracle():
+    """eps, MSE, C*_g, eta (§4.2) of the nine matrices over a range of rho (the Fig. 1 axis),
+    against the oracle's definitions (themselves pinned to Table 4)."""
+    names = catalog.CONFIG2_ORDER
+    mats = [adct.Matrix.from_real(catalog.exact_dct(), "DCT") if n == "DCT" else
+            adct.Matrix.from_int(catalog.INTEGER[n], n) for n in names]
+    rho = torch.tensor([0.1, 0.5, 0.8, 0.95, 0.99], dtype=torch.float64, device=DEV)
+    got = adct.merit_batch(mats, rho).cpu().numpy()
+    for a, n in enumerate(names):
+        chat = M.C if n == "DCT" else M.c_hat(np.array(catalog.INTEGER[n]).reshape(8, 8))
+        for b, r in enumerate(rho.cpu().tolist()):
+            want = [OMR.total_error_energy(chat), OMR.mse_matrix(chat, r), OMR.unified_coding_gain(chat, r),
+                    OMR.transform_efficiency(chat, r)]
+            assert np.allclose(got[a, b], want, rtol=1e-10, atol=1e-12), (n, r, got[a, b], want)
