@@ -144,7 +144,10 @@ constexpr int kWtThreads = 32 * kWtWarps;
 constexpr int kWtBPL = ADCT_WT_BPL;                 // blocks per lane per tile
 constexpr int kWtTileBytes = 2048 * kWtBPL;         // 32 * kWtBPL blocks of 64 bytes
 constexpr int kWtSlots = kWtBPL == 2 ? 3 : 2;       // ring depth (192 KB of shared memory)
-constexpr int kWtChunkTiles = kWtWarps * 8;         // 8 tiles per warp per chunk
+#ifndef ADCT_WT_CHUNK
+#define ADCT_WT_CHUNK 8
+#endif
+constexpr int kWtChunkTiles = kWtWarps * ADCT_WT_CHUNK;  // tiles per warp per chunk x 16 warps
 constexpr size_t kWtSmem = (size_t)kWtWarps * kWtSlots * kWtTileBytes + (size_t)kWtWarps * kWtSlots * 8 + 128;
 
 // tile shape: tw bytes wide (256 = 32 blocks per band, or 128 = 16 blocks) x 4096/tw rows

@@ -1,22 +1,9 @@
 // stream.cu — the hot kernel of BASELINE.json config 4: forward -> zonal retention -> inverse
-// -> squared error per image (§6.1) for uint8 planes, with every
-// 8x8 block read from HBM exactly once through a bulk-copy (TMA engine) ring in shared memory.
+// -> squared error per image (§6.1) for uint8 planes, every 8x8 block
+// read from HBM exactly once through per-warp TMA tile rings in shared memory
+// (fused_u8_wtile_kernel; design, measurements and the issue-bound analysis: DESIGN.md §5.2).
 //
-// Structure (one persistent CTA per SM, 16 warps):
-//  - warp 0 is the producer: one lane streams "stages" (G consecutive 8-row bands of one
-//    image, contiguous in HBM when rows are unpadded) into a ring of shared-memory slots with
-//    cp.async.bulk, completing on a per-slot "full" mbarrier (transaction bytes);
-//  - warps 1..15 (480 threads) are consumers: each thread owns one 8x8 block of the stage at a
-//    time, reads its 8 rows from shared memory (8 x LDS.64, conflict-free: a warp reads 32
-//    consecutive 8-byte words of one row), runs the fused transform in registers, and the warp
-//    arrives on the slot's "empty" mbarrier when done;
-//  - per stage, each consumer warp reduces its blocks' squared error in a fixed shuffle order
-//    and writes one fp64 partial; finalize_kernel adds an image's partials in index order.
-// Registers, not shared memory, bound the in-flight bytes of the old register-prefetch kernel
-// (160 registers, 12 warps/SM, long-scoreboard stalls; profiles/r01_v0_fused_u8_full.txt);
-// here up to 200 KB per SM are in flight and the compute warps never wait on HBM latency.
-//
-// The block computation (block_sse_u8s) is exact-integer fp32 forward Y = T X T^T (all
+// The block computation (block_sse_u8s) is the exact-integer fp32 forward Y = T X T^T (all
 // intermediates are integers < 2^24), weights W = 2/(n_k n_l) folded into the retained
 // coefficients, the inverse x_hat = T^T (W o Y') T of the retained coefficients, and the
 // squared error.  The inverse's last (vertical) butterfly x_hat_i = E_i + O_i,
@@ -24,7 +11,7 @@
 // s_i = x_i + x_{7-i}, t_i = x_i - x_{7-i}:
 //   (x_i - x_hat_i)^2 + (x_{7-i} - x_hat_{7-i})^2 = ((s_i - 2E_i)^2 + (t_i - 2O_i)^2) / 2.
 // For r > 32 the inverse of the dropped coefficients is formed instead (x - x_hat directly,
-// exactly 0 at r = 64; reading A17).  Samples enter fp32 with one PRMT each (pxf).
+// exactly 0 at r = 64; reading A17).  Samples enter fp32 by PRMT (pxf) or I2F.U8 (ubyte).
 #include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -182,143 +169,6 @@ __device__ __forceinline__ float block_sse_u8s(const MP& m, const uint2 (&rows)[
   }
 }
 
-struct StreamArgs {
-  const uint8_t* src;
-  int64_t image_stride, row_stride;  // bytes
-  int32_t width;                     // bytes per row (= W for u8)
-  int32_t bw, bh;                    // blocks per row, bands per image
-  int32_t G, G0, spi, cpi, ns;       // bands per stage / per group, stages and chunks per image, ring slots
-  int64_t n_chunks;
-  int32_t stage_bytes;
-  int32_t contiguous;                // rows of an image unpadded: one copy per stage
-  FastDiv dbw;                       // division by bw
-};
-
-// producer wait on a slot's "empty" barrier: the ring has slack, so sleep between probes
-// instead of spinning on the issue slots the consumer warps need
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  for (;;) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 2000;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    __nanosleep(500);
-  }
-}
-
-// Work unit: a chunk = up to kStreamChunkStages consecutive stages of one image.  CTA b takes
-// chunks b, b + gridDim.x, ...; the per-(chunk, consumer warp) fp64 partial is grid-independent.
-template <class MP, int R>
-__global__ void __launch_bounds__(kStreamThreads, 1)
-    fused_u8_stream_kernel(StreamArgs a, DevMat dm, double* __restrict__ partial, uint32_t magic) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint8_t* ring = smem_raw;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (int64_t)a.ns * a.stage_bytes);
-  uint64_t* empty = full + a.ns;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < a.ns; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kStreamConsumerWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    // ---- producer --------------------------------------------------------------------------
-    if (lane == 0) {
-      int slot = 0;
-      uint32_t phase = 0;  // parity of the slot's current round
-      uint32_t k = 0;
-      for (int64_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
-        const int64_t img = cg / a.cpi;
-        const int32_t st0 = (int32_t)(cg - img * a.cpi) * kStreamChunkStages;
-        const int32_t st1 = min(a.spi, st0 + kStreamChunkStages);
-        const uint8_t* isrc = a.src + img * a.image_stride;
-        for (int32_t stg = st0; stg < st1; ++stg, ++k) {
-          if (k >= (uint32_t)a.ns) mbar_wait_sleep(&empty[slot], phase ^ 1u);
-          const int32_t b0 = stg * a.G;
-          const int32_t nb = min(a.G, a.bh - b0);
-          const uint32_t bytes = (uint32_t)nb * 8u * (uint32_t)a.width;
-          uint8_t* dst = ring + (int64_t)slot * a.stage_bytes;
-          const uint8_t* src = isrc + (int64_t)b0 * 8 * a.row_stride;
-          mbar_arrive_expect_tx(&full[slot], bytes);
-          if (a.contiguous) {
-            bulk_g2s(dst, src, bytes, &full[slot]);
-          } else {
-            for (int r = 0; r < nb * 8; ++r)
-              bulk_g2s(dst + (int64_t)r * a.width, src + (int64_t)r * a.row_stride, (uint32_t)a.width, &full[slot]);
-          }
-          if (++slot == a.ns) { slot = 0; phase ^= 1u; }
-        }
-      }
-    }
-    return;
-  }
-
-  // ---- consumers ------------------------------------------------------------------------------
-  const MP m(dm);
-  const int ct = threadIdx.x - 32;          // 0 .. 479
-  const int cw = warp - 1;                  // consumer warp 0 .. 14
-  const uint32_t ring_u32 = smem_u32(ring);
-  const uint32_t W = (uint32_t)a.width;
-  // fixed mapping (bw divides the consumer count): this thread's block in every group of G0 bands
-  const uint32_t gband = a.G0 ? (uint32_t)ct / (uint32_t)a.bw : 0u;
-  const uint32_t toff = a.G0 ? gband * 8u * W + ((uint32_t)ct - gband * (uint32_t)a.bw) * 8u : 0u;
-  const uint32_t gstep = (uint32_t)a.G0 * 8u * W;
-  int slot = 0;
-  uint32_t phase = 0;
-  for (int64_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
-    const int64_t img = cg / a.cpi;
-    const int32_t st0 = (int32_t)(cg - img * a.cpi) * kStreamChunkStages;
-    const int32_t st1 = min(a.spi, st0 + kStreamChunkStages);
-    float acc = 0.0f;
-    for (int32_t stg = st0; stg < st1; ++stg) {
-      const int32_t nb = min(a.G, a.bh - stg * a.G);
-      mbar_wait(&full[slot], phase);
-      const uint32_t base = ring_u32 + (uint32_t)slot * (uint32_t)a.stage_bytes;
-      if (a.G0) {
-        uint32_t p = base + toff;
-        for (int32_t g0 = 0; g0 < nb; g0 += a.G0, p += gstep) {
-          if ((int32_t)gband < nb - g0) {
-            uint2 rows[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)i * W);
-            acc += block_sse_u8s<MP, R>(m, rows, magic);
-          }
-        }
-      } else {
-        const int32_t nblk = nb * a.bw;
-        for (int32_t q = ct; q < nblk; q += kStreamConsumers) {
-          const uint32_t band = fdiv((uint32_t)q, a.dbw);
-          const uint32_t bx = (uint32_t)q - band * (uint32_t)a.bw;
-          const uint32_t p = base + band * 8u * W + bx * 8u;
-          uint2 rows[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)i * W);
-          acc += block_sse_u8s<MP, R>(m, rows, magic);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == a.ns) { slot = 0; phase ^= 1u; }
-    }
-    // per-(chunk, warp) partial, fixed shuffle order
-    double v = (double)acc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) partial[cg * kStreamConsumerWarps + cw] = v;
-  }
-}
-
 // ---- warp-tile kernel ----------------------------------------------------------------------------
 struct WtArgs {
   int32_t tpb, tpi, cpi;  // tiles per band pair / per image, chunks per image
@@ -410,35 +260,44 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   for (int s = 0; s < kWtSlots; ++s)
     if (pf.cg < a.n_chunks) issue(s);
 
-  // lane -> block column (lane % BPR) and its kWtBPL bands kWtBPL*(lane / BPR) + b
-  const uint32_t lane_u32 = ring0 + (uint32_t)(lane % BPR) * 8u + (uint32_t)(lane / BPR) * (8u * kWtBPL) * TW;
+  // lane -> block column (lane % BPR) and its two bands 2*(lane / BPR), 2*(lane / BPR) + 1
+  const uint32_t lane_u32 = ring0 + (uint32_t)(lane % BPR) * 8u + (uint32_t)(lane / BPR) * 16u * TW;
   int slot = 0;
   uint32_t phase = 0;
-  for (uint32_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
-    const uint32_t img = fdiv(cg, a.dcpi);
-    const int32_t n = min(kWtChunkTiles, a.tpi - (int32_t)(cg - img * (uint32_t)a.cpi) * kWtChunkTiles);
-    float acc = 0.0f;
-    for (int32_t j = w; j < n; j += kWtWarps) {  // this warp's tiles of the chunk
-      mbar_wait(&wfull[slot], phase);
-      const uint32_t p = lane_u32 + (uint32_t)slot * kWtTileBytes;
+  WtIt it;
+  it.cg = blockIdx.x;
+  wt_enter(a, w, it);
+  float acc = 0.0f;
+  // chunks in which this warp has no tile keep a zero partial
+  if (lane == 0)
+    for (uint32_t cz = blockIdx.x; cz < min(it.cg, a.n_chunks); cz += gridDim.x) partial[(int64_t)cz * kWtWarps + w] = 0.0;
+  while (it.cg < a.n_chunks) {
+    mbar_wait(&wfull[slot], phase);
+    const uint32_t p = lane_u32 + (uint32_t)slot * kWtTileBytes;
 #pragma unroll kWtUnroll
-      for (int b = 0; b < kWtBPL; ++b) {  // the lane's blocks (consecutive bands of the tile)
-        uint2 rows[8];
+    for (int b = 0; b < 2; ++b) {  // the lane's two blocks (consecutive bands of the tile)
+      uint2 rows[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)(b * 8 + i) * TW);
-        acc += block_sse_u8s<MP, R>(m, rows, magic);
-      }
-      __syncwarp();
-      // the slot was read through the generic proxy; order that before the async-proxy refill
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (pf.cg < a.n_chunks) issue(slot);
-      if (++slot == kWtSlots) { slot = 0; phase ^= 1u; }
+      for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)(b * 8 + i) * TW);
+      acc += block_sse_u8s<MP, R>(m, rows, magic);
     }
-    // per-(chunk, warp) partial in a fixed shuffle order (0 when the warp had no tile)
-    double v = (double)acc;
+    __syncwarp();
+    // the slot was read through the generic proxy; order that before the async-proxy refill
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (pf.cg < a.n_chunks) issue(slot);
+    if (++slot == kWtSlots) { slot = 0; phase ^= 1u; }
+    const uint32_t cg = it.cg;
+    if (wt_next(a, w, it)) {  // chunk done: per-(chunk, warp) partial in a fixed shuffle order
+      double v = (double)acc;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) partial[(int64_t)cg * kWtWarps + w] = v;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        partial[(int64_t)cg * kWtWarps + w] = v;
+        for (uint32_t cz = cg + gridDim.x; cz < min(it.cg, a.n_chunks); cz += gridDim.x)
+          partial[(int64_t)cz * kWtWarps + w] = 0.0;
+      }
+      acc = 0.0f;
+    }
   }
 }
 
@@ -466,21 +325,6 @@ int sms_s() {
   return g_sms_s;
 }
 
-template <class MP, int R>
-bool launch_stream_r(const StreamArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
-  const size_t smem = (size_t)a.ns * a.stage_bytes + 2 * sizeof(uint64_t) * a.ns;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(fused_u8_stream_kernel<MP, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(kStreamSmemBudget + 1024));
-  });
-  if (attr_err != cudaSuccess) return false;
-  const int64_t grid = a.n_chunks < sms_s() ? a.n_chunks : sms_s();
-  fused_u8_stream_kernel<MP, R><<<(unsigned)grid, kStreamThreads, smem, st>>>(a, dm, partial, 0x47000000u);
-  return true;
-}
-
 template <class MP, int R, int TW>
 bool launch_wtile_rt(const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
   static std::once_flag once;
@@ -505,8 +349,9 @@ bool launch_wtile_r(int tw, const CUtensorMap& map, const WtArgs& a, const DevMa
   return tw == 256 && launch_wtile_rt<MP, R, 256>(map, a, dm, partial, st);
 }
 
-// compiled (matrix, r) pairs: the paper's T1 at the r values of the paper's figures and
-// BASELINE.json configs, runtime matrices at config 4's r = 10; other pairs use the r-sweep kernel
+// compiled (matrix, r) pairs: the paper's T1 at config 4's r = 10 and the r of the paper's
+// Lena figures (3, 14), runtime matrices at r = 10; other pairs take the generic
+// fused kernels (each instantiation of this kernel costs minutes of front-end compile time)
 template <class MP>
 bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial,
                   cudaStream_t st) {
@@ -517,27 +362,12 @@ bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const 
 #define ADCT_WT_CASE(R) \
   case R:               \
     return launch_wtile_r<MP, R>(tw, map, a, dm, partial, st);
-      ADCT_WT_CASE(1) ADCT_WT_CASE(3) ADCT_WT_CASE(6) ADCT_WT_CASE(10) ADCT_WT_CASE(14)
-      ADCT_WT_CASE(15) ADCT_WT_CASE(21) ADCT_WT_CASE(28) ADCT_WT_CASE(36)
+      ADCT_WT_CASE(3) ADCT_WT_CASE(10) ADCT_WT_CASE(14)
 #undef ADCT_WT_CASE
       default:
         return false;
     }
   }
-}
-
-const int g_stream_mode = [] {  // ADCT_STREAM_MODE=stage selects the stage-ring kernel
-  const char* e = std::getenv("ADCT_STREAM_MODE");
-  return (e && e[0] == 's') ? 1 : 0;
-}();
-
-// the stage-ring kernel is kept for A/B comparison at the headline configuration only
-template <class MP>
-bool launch_stream(int r, const StreamArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
-  if constexpr (MP::kConst) {
-    if (r == 10) return launch_stream_r<MP, 10>(a, dm, partial, st);
-  }
-  return false;
 }
 
 }  // namespace
@@ -547,7 +377,7 @@ bool launch_stream(int r, const StreamArgs& a, const DevMat& dm, double* partial
 // On success the per-image SSE is in sse[n_images] (finalize launched on st).
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
                      double* partial, cudaStream_t st, adct_status* status) {
-  if (g_stream_mode == 0) {
+  {
     WtPlan p = wt_plan(g);
     if (!p.ok || g.n_images == 0 || !aligned(src, 16)) return false;
     if (!m->specialized && p.tw != 256) {  // runtime matrices: 256-byte tiles only
@@ -579,36 +409,7 @@ bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& 
     *status = launch_status();
     return true;
   }
-  const StreamPlan p = stream_plan(g);
-  if (!p.ok || g.n_images == 0) return false;
-  if (!aligned(src, 16)) return false;
-  StreamArgs a;
-  a.src = src;
-  a.image_stride = g.image_stride;
-  a.row_stride = g.row_stride;
-  a.width = g.width;
-  a.bw = g.width / 8;
-  a.bh = g.height / 8;
-  a.G = p.G;
-  a.G0 = p.G0;
-  a.spi = p.spi;
-  a.cpi = p.cpi;
-  a.ns = p.stages_in_ring;
-  a.n_chunks = p.n_chunks;
-  a.stage_bytes = (int32_t)p.stage_bytes;
-  a.contiguous = (g.row_stride == g.width) ? 1 : 0;
-  a.dbw = make_fastdiv((uint32_t)a.bw);
-  const bool ok = m->specialized ? launch_stream<T1Mat>(r, a, m->dev, partial, st)
-                                 : launch_stream<RtMat>(r, a, m->dev, partial, st);
-  if (!ok) return false;
-  count_launch();
-  if ((*status = launch_status()) != ADCT_OK) return true;
-  SlotMap sm{};
-  sm.s[0] = 0;
-  launch_finalize(partial, p.cpi * kStreamConsumerWarps, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0,
-                  sse, nullptr, st);
-  *status = launch_status();
-  return true;
+  return false;
 }
 
 }  // namespace adct
