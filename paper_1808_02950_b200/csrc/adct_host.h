@@ -145,7 +145,7 @@ constexpr int kWtBPL = ADCT_WT_BPL;                 // blocks per lane per tile
 constexpr int kWtTileBytes = 2048 * kWtBPL;         // 32 * kWtBPL blocks of 64 bytes
 constexpr int kWtSlots = kWtBPL == 2 ? 3 : 2;       // ring depth (192 KB of shared memory)
 #ifndef ADCT_WT_CHUNK
-#define ADCT_WT_CHUNK 8
+#define ADCT_WT_CHUNK 16
 #endif
 constexpr int kWtChunkTiles = kWtWarps * ADCT_WT_CHUNK;  // tiles per warp per chunk x 16 warps
 constexpr size_t kWtSmem = (size_t)kWtWarps * kWtSlots * kWtTileBytes + (size_t)kWtWarps * kWtSlots * 8 + 128;
