@@ -12,12 +12,20 @@ constexpr int NT = 32;  // one warp per CTA: small images still spread over ever
 // Coefficients are added in decreasing zig-zag rank z = 63..1; after adding rank z the
 // register block e = H (W o Y o [rank >= z]) H^T is x - x_hat for r = z.  Each step is a
 // rank-one update e += (w y)_z h_k h_l^T (the inverse applied to one coefficient).
-template <typename SrcT, class MP>
+// zig-zag position of rank z (reading A5), for the rolled loop below
+__constant__ int8_t c_zz[64];
+
+// The rank loop is rolled (runtime coefficient position): an unrolled 63-step body is
+// ~10^4 instructions and thrashed the instruction cache (ncu: 72% "no instruction" stalls).
+// The matrix comes from kernel parameters for every matrix, T1 included: products by 0 and +-1
+// are exact in fp32, so the sums are the same as with the compile-time network.
+template <typename SrcT>
 __global__ void __launch_bounds__(NT) fused_sweep_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm,
                                                          FastDiv dbw, int32_t chunks, int32_t bpt, uint64_t rmask,
                                                          int32_t rmin, int clip, double* __restrict__ partial) {
   __shared__ float zacc[64][NT];
-  const MP m(dm);
+  __shared__ float ys[64][NT];
+  const RtMat m(dm);
 #pragma unroll
   for (int z = 0; z < 64; ++z) zacc[z][threadIdx.x] = 0.0f;
   const SrcT* base = src + (int64_t)blockIdx.y * g.image_stride;
@@ -28,27 +36,34 @@ __global__ void __launch_bounds__(NT) fused_sweep_kernel(const SrcT* __restrict_
     if (q >= g.nbi) break;
     typename Src<SrcT>::Row rows[8];
     load_rows(base, g, dbw, q, rows);
-    float x[8][8], y[8][8], e[8][8];
+    float x[8][8], e[8][8];
+    {
+      float y[8][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) Src<SrcT>::to_f(rows[i], x[i]);
-    fwd2d(m, x, y);
+      for (int i = 0; i < 8; ++i) Src<SrcT>::to_f(rows[i], x[i]);
+      fwd2d(m, x, y);
+#pragma unroll
+      for (int p = 0; p < 64; ++p) ys[p][threadIdx.x] = y[p >> 3][p & 7] * dm.wy[p];
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) e[i][j] = 0.0f;
-#pragma unroll
-    for (int zr = 63; zr >= 1; --zr) {
-      if (zr < rmin) break;
-      const int pos = zz_order_at(zr);
+#pragma unroll 1
+    for (int zr = 63; zr >= rmin && zr >= 1; --zr) {
+      const int pos = c_zz[zr];
       const int k = pos >> 3, l = pos & 7;
-      const float c = y[k][l] * m.wy(k, l);
-      float a[8];
+      const float c = ys[pos][threadIdx.x];
+      float a[8], hl[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = fmac<MP>(m.h(i, k), c, -0.0f);
+      for (int i = 0; i < 8; ++i) {
+        a[i] = fmaf(dm.h[i * 8 + k], c, -0.0f);
+        hl[i] = dm.h[i * 8 + l];
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) e[i][j] = fmac<MP>(m.h(j, l), a[i], e[i][j]);
+        for (int j = 0; j < 8; ++j) e[i][j] = fmaf(hl[j], a[i], e[i][j]);
       if ((rmask >> zr) & 1ull) {
         float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         if (clip == ADCT_CLIP_NONE) {
@@ -101,14 +116,19 @@ void launch_sweep_any(bool u8, bool specialized, int clip, cudaStream_t st, cons
                       double* partial) {
   const int32_t chunks = (int32_t)sweep_chunks(g), bpt = sweep_bpt(g);
   const dim3 grid((unsigned)chunks, (unsigned)g.n_images);
-#define ADCT_SWEEP_C(T, MP) \
-  fused_sweep_kernel<T, MP><<<grid, NT, 0, st>>>((const T*)src, kg, dm, dbw, chunks, bpt, rmask, rmin, clip, partial);
-  if (u8) {
-    if (specialized) { ADCT_SWEEP_C(uint8_t, T1Mat) } else { ADCT_SWEEP_C(uint8_t, RtMat) }
-  } else {
-    if (specialized) { ADCT_SWEEP_C(int16_t, T1Mat) } else { ADCT_SWEEP_C(int16_t, RtMat) }
-  }
-#undef ADCT_SWEEP_C
+  (void)specialized;
+  static bool zz_ready = [] {
+    int8_t zz[64];
+    for (int z = 0; z < 64; ++z) zz[z] = (int8_t)kZZ.order[z];
+    return cudaMemcpyToSymbol(c_zz, zz, sizeof(zz)) == cudaSuccess;
+  }();
+  (void)zz_ready;
+  if (u8)
+    fused_sweep_kernel<uint8_t><<<grid, NT, 0, st>>>((const uint8_t*)src, kg, dm, dbw, chunks, bpt, rmask, rmin, clip,
+                                                     partial);
+  else
+    fused_sweep_kernel<int16_t><<<grid, NT, 0, st>>>((const int16_t*)src, kg, dm, dbw, chunks, bpt, rmask, rmin, clip,
+                                                     partial);
 }
 
 }  // namespace adct
