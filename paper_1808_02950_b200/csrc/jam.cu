@@ -75,7 +75,10 @@ struct JamW {
   float w[N * N];  // keep_kl / (d_k d_l)
 };
 
-// N samples of one row as fp32 (16-byte vector loads; rows are 16-byte aligned)
+// N samples of one row as fp32 (16-byte vector loads; rows are 16-byte aligned).  Conversions
+// avoid the quarter-rate XU pipe (I2F/F2I): a u8 sample is placed in the mantissa of 2^23 by one
+// PRMT and the 2^23 removed by an FADD; an int16 sample is sign-extended (PRMT / SHF) and
+// converted by I2FP on the ALU pipe; results are rounded with the 1.5*2^23 trick.
 template <int N>
 __device__ __forceinline__ void load_row(const uint8_t* p, float* x) {
 #pragma unroll
@@ -83,7 +86,8 @@ __device__ __forceinline__ void load_row(const uint8_t* p, float* x) {
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + c);
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int q = 0; q < 16; ++q) x[c * 16 + q] = (float)((w[q >> 2] >> (8 * (q & 3))) & 0xffu);
+    for (int q = 0; q < 16; ++q)
+      x[c * 16 + q] = __uint_as_float(__byte_perm(w[q >> 2], 0x4B000000u, 0x7440u | (uint32_t)(q & 3))) - 8388608.0f;
   }
 }
 template <int N>
@@ -93,9 +97,15 @@ __device__ __forceinline__ void load_row(const int16_t* p, float* x) {
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + c);
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int q = 0; q < 8; ++q) x[c * 8 + q] = (float)(int16_t)((w[q >> 1] >> (16 * (q & 1))) & 0xffffu);
+    for (int q = 0; q < 4; ++q) {
+      x[c * 8 + 2 * q] = (float)(int32_t)__byte_perm(w[q], 0u, 0x9910u);  // sign-extended low half
+      x[c * 8 + 2 * q + 1] = (float)((int32_t)w[q] >> 16);
+    }
   }
 }
+
+// low 16 (or 8) bits of 1.5*2^23 + v: v rounded half to even, two's complement
+__device__ __forceinline__ uint32_t rbits(float v) { return __float_as_uint(v + 12582912.0f); }
 
 template <int N>
 __device__ __forceinline__ void store_row_any(void* recon, int64_t off, int out_t, const float* x) {
@@ -103,14 +113,13 @@ __device__ __forceinline__ void store_row_any(void* recon, int64_t off, int out_
     float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(recon) + off);
 #pragma unroll
     for (int c = 0; c < N / 4; ++c) o[c] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
-  } else if (out_t == ADCT_I16) {
+  } else if (out_t == ADCT_I16) {  // x already rounded and saturated (CLIP_ROUND)
     uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<int16_t*>(recon) + off);
 #pragma unroll
     for (int c = 0; c < N / 8; ++c) {
       uint32_t w[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        w[q] = (uint32_t)(uint16_t)(int16_t)x[8 * c + 2 * q] | ((uint32_t)(uint16_t)(int16_t)x[8 * c + 2 * q + 1] << 16);
+      for (int q = 0; q < 4; ++q) w[q] = __byte_perm(rbits(x[8 * c + 2 * q]), rbits(x[8 * c + 2 * q + 1]), 0x5410u);
       o[c] = make_uint4(w[0], w[1], w[2], w[3]);
     }
   } else {
@@ -119,9 +128,11 @@ __device__ __forceinline__ void store_row_any(void* recon, int64_t off, int out_
     for (int c = 0; c < N / 16; ++c) {
       uint32_t w[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        w[q] = (uint32_t)(uint8_t)x[16 * c + 4 * q] | ((uint32_t)(uint8_t)x[16 * c + 4 * q + 1] << 8) |
-               ((uint32_t)(uint8_t)x[16 * c + 4 * q + 2] << 16) | ((uint32_t)(uint8_t)x[16 * c + 4 * q + 3] << 24);
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t lo = __byte_perm(rbits(x[16 * c + 4 * q]), rbits(x[16 * c + 4 * q + 1]), 0x0040u);
+        const uint32_t hi = __byte_perm(rbits(x[16 * c + 4 * q + 2]), rbits(x[16 * c + 4 * q + 3]), 0x0040u);
+        w[q] = __byte_perm(lo, hi, 0x5410u);
+      }
       o[c] = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
@@ -185,7 +196,7 @@ __global__ void __launch_bounds__(kJamNT) jam_roundtrip_kernel(const SrcT* __res
         for (int j = 0; j < N; ++j) {
           float v = x[j];
           if (clip != ADCT_CLIP_NONE) v = fminf(fmaxf(v, lo), hi);
-          if (clip == ADCT_CLIP_ROUND) v = rintf(v);
+          if (clip == ADCT_CLIP_ROUND && out_t == ADCT_F32) v = rintf(v);  // integer stores round themselves
           x[j] = v;
         }
         store_row_any<N>(recon, off, out_t, x);
