@@ -468,10 +468,11 @@ def main():
     luma_bytes = FRAMES * (H // 8) * (W // 8) * 64
     hbm_peak, peak_kind = peaks()
     achieved = luma_bytes / (luma_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, ipb = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get("fused_u8_kernel_bytes_per_launch")
+            nt = json.load(f)
+            traffic, ipb = nt.get("fused_u8_kernel_bytes_per_launch"), nt.get("instructions_per_block")
     except Exception:
         pass
 
@@ -521,6 +522,16 @@ def main():
                          "kernel": "fused_u8_wtile_kernel<T1Mat,10> + finalize_kernel (luma plane, 66,355,200 blocks x 64 B)",
                          "kernel_ms": luma_ms},
             "clocks": clk.summary(),
+            # the binding constraint of the hot kernel: one warp-instruction per
+            # clock per SMSP; roof = SMs x 4 x clock x 32 lanes / (SASS instructions per block)
+            "issue_roofline": None if not ipb else {
+                "instructions_per_block": ipb,
+                "roof_blocks_per_s": torch.cuda.get_device_properties(dev).multi_processor_count * 4 *
+                                     (clk.summary()["sm_mhz"] or 1965) * 1e6 * 32 / ipb,
+                "achieved_blocks_per_s": FRAMES * (H // 8) * (W // 8) / (luma_ms * 1e-3),
+                "frac": FRAMES * (H // 8) * (W // 8) / (luma_ms * 1e-3) /
+                        (torch.cuda.get_device_properties(dev).multi_processor_count * 4 *
+                         (clk.summary()["sm_mhz"] or 1965) * 1e6 * 32 / ipb)},
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(const double* __restri
 // shared memory, horizontal 8-sums of x, y, x^2, y^2, xy are formed per row, then vertical
 // 8-sums per position, all in fp64; per-CTA sums of the window SSIMs are reduced in a fixed
 // order and finalize_kernel averages an image's tiles in index order.
-constexpr int kSsimT = 32, kSsimIn = kSsimT + 7, kSsimNT = 256;
+constexpr int kSsimT = 32, kSsimIn = kSsimT + 7, kSsimNT = 256, kSsimSeg = 4;  // positions per running-sum segment
 
 template <typename OrigT, typename RecT>
 __global__ void __launch_bounds__(kSsimNT) ssim_kernel(const OrigT* __restrict__ orig, const RecT* __restrict__ rec,
@@ -317,40 +317,65 @@ __global__ void __launch_bounds__(kSsimNT) ssim_kernel(const OrigT* __restrict__
     sy[r * 40 + c] = b;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kSsimIn * kSsimT; i += kSsimNT) {
-    const int r = i / kSsimT, c = i % kSsimT;
+  // horizontal 8-sums as running sums along row segments of 8 positions
+  for (int it = threadIdx.x; it < kSsimIn * (kSsimT / kSsimSeg); it += kSsimNT) {
+    const int r = it / (kSsimT / kSsimSeg), c0 = (it % (kSsimT / kSsimSeg)) * kSsimSeg;
+    const float* px = sx + r * 40;
+    const float* py = sy + r * 40;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const double a = sx[r * 40 + c + k], b = sy[r * 40 + c + k];
+      const double a = px[c0 + k], b = py[c0 + k];
       s0 += a;
       s1 += b;
       s2 = fma(a, a, s2);
       s3 = fma(b, b, s3);
       s4 = fma(a, b, s4);
     }
-    hs[0 * kSsimIn * kSsimT + i] = s0;
-    hs[1 * kSsimIn * kSsimT + i] = s1;
-    hs[2 * kSsimIn * kSsimT + i] = s2;
-    hs[3 * kSsimIn * kSsimT + i] = s3;
-    hs[4 * kSsimIn * kSsimT + i] = s4;
+#pragma unroll
+    for (int c = c0; c < c0 + kSsimSeg; ++c) {
+      if (c > c0) {  // slide the window by one: add sample c+7, drop sample c-1
+        const double a = px[c + 7], b = py[c + 7], a0 = px[c - 1], b0 = py[c - 1];
+        s0 += a - a0;
+        s1 += b - b0;
+        s2 += fma(a, a, -a0 * a0);
+        s3 += fma(b, b, -b0 * b0);
+        s4 += fma(a, b, -a0 * b0);
+      }
+      const int i = r * kSsimT + c;
+      hs[0 * kSsimIn * kSsimT + i] = s0;
+      hs[1 * kSsimIn * kSsimT + i] = s1;
+      hs[2 * kSsimIn * kSsimT + i] = s2;
+      hs[3 * kSsimIn * kSsimT + i] = s3;
+      hs[4 * kSsimIn * kSsimT + i] = s4;
+    }
   }
   __syncthreads();
+  // vertical 8-sums as running sums down column segments of 8 positions, then the window SSIM
   double acc = 0.0;
-  for (int i = threadIdx.x; i < kSsimT * kSsimT; i += kSsimNT) {
-    const int r = i / kSsimT, c = i % kSsimT;
-    if (y0 + r + 8 > height || x0 + c + 8 > width) continue;
+  for (int it = threadIdx.x; it < kSsimT * (kSsimT / kSsimSeg); it += kSsimNT) {
+    const int c = it % kSsimT, r0 = (it / kSsimT) * kSsimSeg;
     double v[5];
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
       double t = 0.0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) t += hs[q * kSsimIn * kSsimT + (r + k) * kSsimT + c];
-      v[q] = t * (1.0 / 64.0);
+      for (int k = 0; k < 8; ++k) t += hs[q * kSsimIn * kSsimT + (r0 + k) * kSsimT + c];
+      v[q] = t;
     }
-    const double mx = v[0], my = v[1];
-    const double vx = v[2] - mx * mx, vy = v[3] - my * my, cxy = v[4] - mx * my;
-    acc += ((2.0 * mx * my + c1) * (2.0 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2));
+#pragma unroll
+    for (int r = r0; r < r0 + kSsimSeg; ++r) {
+      if (r > r0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+          v[q] += hs[q * kSsimIn * kSsimT + (r + 7) * kSsimT + c] - hs[q * kSsimIn * kSsimT + (r - 1) * kSsimT + c];
+      }
+      if (y0 + r + 8 > height || x0 + c + 8 > width) continue;
+      const double mx = v[0] * (1.0 / 64.0), my = v[1] * (1.0 / 64.0);
+      const double vx = v[2] * (1.0 / 64.0) - mx * mx, vy = v[3] * (1.0 / 64.0) - my * my;
+      const double cxy = v[4] * (1.0 / 64.0) - mx * my;
+      acc += ((2.0 * mx * my + c1) * (2.0 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2));
+    }
   }
   const double tot = block_sum<kSsimNT>(acc, red);
   if (threadIdx.x == 0) partial[(int64_t)img * tiles + blockIdx.x] = tot;
