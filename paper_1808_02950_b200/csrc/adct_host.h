@@ -64,7 +64,6 @@ inline KGeom make_kgeom(const adct_geom& g) {
 // number of CTAs per image of the two-level deterministic reductions
 constexpr int kRedNT = 128;   // threads per CTA
 constexpr int kFusedBPT = 8;    // blocks per thread, generic fused kernels
-constexpr int kFusedBPTU8 = 9;  // blocks per thread, hot u8 kernel (3-deep prefetch ring)
 inline int64_t fused_chunks(const adct_geom& g, int bpt = kFusedBPT) {
   const int64_t nbi = (int64_t)(g.height / 8) * (g.width / 8);
   const int64_t per = (int64_t)kRedNT * bpt;
@@ -73,61 +72,6 @@ inline int64_t fused_chunks(const adct_geom& g, int bpt = kFusedBPT) {
 constexpr int kSseRows = 8;  // image rows per CTA in psnr_reduce
 inline int64_t sse_chunks(const adct_geom& g) { return (g.height + kSseRows - 1) / kSseRows; }
 
-// ---- streaming (bulk-copy staged) fused kernel: stage plan ------------------------------------
-// A "band" is the 8 image rows of one block row.  A stage is G consecutive bands of ONE image,
-// copied global -> shared memory with cp.async.bulk and consumed by kStreamConsumers threads,
-// one 8x8 block per thread per pass.  Per-(stage, consumer warp) fp64 partials make the
-// per-image sums independent of the grid (and of how images are sharded over GPUs).
-constexpr int kStreamWarps = 16;                    // 1 producer warp + 15 consumer warps
-constexpr int kStreamThreads = 32 * kStreamWarps;
-constexpr int kStreamConsumerWarps = kStreamWarps - 1;
-constexpr int kStreamConsumers = 32 * kStreamConsumerWarps;  // 480
-constexpr int64_t kStreamSmemBudget = 200 * 1024;   // stage ring (of 227 KB per CTA)
-constexpr int64_t kStreamStageTargetDefault = 32 * 1024;
-// stage-size target in bytes (env ADCT_STREAM_STAGE_KB overrides, for tuning runs)
-int64_t stream_stage_target();
-constexpr int32_t kStreamChunkStages = 8;           // stages per partial-sum chunk
-
-struct StreamPlan {
-  int32_t G;            // bands per stage
-  int32_t G0;           // bands per "group" of one block per consumer (0: no fixed mapping)
-  int32_t spi;          // stages per image
-  int32_t cpi;          // chunks per image (kStreamChunkStages stages each, the last partial)
-  int32_t stages_in_ring;
-  int64_t stage_bytes;  // G * 8 * W (bytes of one full stage)
-  int64_t n_chunks;     // n_images * cpi
-  bool ok;              // geometry supported by the streaming kernel
-};
-
-inline StreamPlan stream_plan(const adct_geom& g, int esz = 1) {
-  StreamPlan p{};
-  const int64_t W = (int64_t)g.width * esz, bw = g.width / 8, bh = g.height / 8;
-  if (bw <= 0 || bh <= 0) return p;
-  int64_t G;
-  if (kStreamConsumers % bw == 0) {
-    p.G0 = (int32_t)(kStreamConsumers / bw);  // one block per consumer thread per group
-    int64_t k = stream_stage_target() / (p.G0 * 8 * W);
-    if (k < 1) k = 1;
-    G = p.G0 * k;
-  } else {
-    G = stream_stage_target() / (8 * W);
-    if (G < 1) G = 1;
-  }
-  if (G > bh) G = bh;
-  p.G = (int32_t)G;
-  p.spi = (int32_t)((bh + G - 1) / G);
-  p.cpi = (p.spi + kStreamChunkStages - 1) / kStreamChunkStages;
-  p.stage_bytes = G * 8 * W;
-  p.stages_in_ring = (int32_t)(kStreamSmemBudget / p.stage_bytes);
-  if (p.stages_in_ring > 8) p.stages_in_ring = 8;
-  p.n_chunks = g.n_images * (int64_t)p.cpi;
-  // bulk copies move 16-byte multiples between 16-byte aligned addresses; the mbarrier
-  // transaction count of one stage must stay below 2^20
-  p.ok = p.stages_in_ring >= 2 && (W % 16) == 0 && ((int64_t)g.row_stride * esz) % 16 == 0 &&
-         ((int64_t)g.image_stride * esz) % 16 == 0 && p.stage_bytes < (1 << 20) &&
-         p.n_chunks < ((int64_t)1 << 31);
-  return p;
-}
 // ---- warp-tile streaming kernel (the default hot kernel) ---------------------------------------
 // Every warp owns a private ring of kWtSlots tiles.  A tile is 16 image rows x 256 bytes (two
 // bands of 32 horizontally adjacent 8x8 blocks: 2 blocks per lane), fetched by ONE TMA tensor
@@ -185,8 +129,7 @@ inline WtPlan wt_plan(const adct_geom& g) {
 }
 
 inline int64_t stream_partials_per_image(const adct_geom& g) {
-  const StreamPlan p = stream_plan(g);
-  int64_t best = (int64_t)p.cpi * kStreamConsumerWarps;
+  int64_t best = 0;
   for (int tw : {256, 128}) {  // either warp-tile shape may be used (runtime matrices: 256 only)
     const int64_t rows = kWtTileBytes / tw;
     const int64_t tpi = ((g.width + tw - 1) / tw) * ((g.height + rows - 1) / rows);

@@ -18,14 +18,6 @@ std::atomic<int64_t> g_launches{0};
 int64_t sweep_chunks(const adct_geom& g);
 int64_t ssim_tiles(const adct_geom& g);
 
-int64_t stream_stage_target() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("ADCT_STREAM_STAGE_KB");
-    const long kb = e ? std::atol(e) : 0;
-    return kb > 0 ? (int64_t)kb * 1024 : kStreamStageTargetDefault;
-  }();
-  return v;
-}
 
 namespace {
 
