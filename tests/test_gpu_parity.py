@@ -523,3 +523,33 @@ def test_merit_batch_matches_oracle():
             want = [OMR.total_error_energy(chat), OMR.mse_matrix(chat, r), OMR.unified_coding_gain(chat, r),
                     OMR.transform_efficiency(chat, r)]
             assert np.allclose(got[a, b], want, rtol=1e-10, atol=1e-12), (n, r, got[a, b], want)
+
+
+# --- full-size configurations in the bench's launch configuration (sampled outputs) ----------------
+
+def test_config3_full_size_sampled(mats):
+    """BASELINE config 3: 1024 frames 1920x1080 (+U(-4,4)) through the TMA quantiser in one
+    call; frames 0, 511 and 1023 bit-exact against the oracle's integer rule."""
+    imgs = synth.ar1_stack(1024, 1080, 1920, 0.95, seed=3, device=DEV, noise_uniform=4.0, batch=16)
+    q = adct.approx_dct8x8_fwd_quant(mats["T1"], imgs, 16)
+    n, _ = oracle.row_scaling(M.T1)
+    for f in (0, 511, 1023):
+        x = imgs[f:f + 1].cpu().numpy()
+        assert np.array_equal(q[f:f + 1].cpu().numpy(), oracle.quantize(oracle.forward_int(M.T1, x), n, 16))
+    del imgs, q
+    torch.cuda.empty_cache()
+
+
+def test_config5_large_roundtrip_sampled(mats):
+    """BASELINE config 5 at 2^24 blocks (the bench runs 2^26): the whole stack round-trips
+    bit-exactly at r = 64; sampled blocks at r = 10 against the oracle reconstruction."""
+    nb = 1 << 24
+    x = synth.laplace_blocks(nb, seed=5, device=DEV).reshape(nb, 8, 8)
+    assert torch.equal(adct.approx_dct8x8_roundtrip(mats["T1"], x, 64, torch.int16), x)
+    rec = adct.approx_dct8x8_roundtrip(mats["T1"], x, 10, torch.float32)
+    idx = torch.tensor([0, 12345, nb // 2, nb - 1], device=DEV)
+    got = rec[idx].cpu().numpy()
+    ref = _oracle_recon("T1", x[idx].cpu().numpy(), 10)
+    assert rel_block_err(got, ref) <= RTOL
+    del x, rec
+    torch.cuda.empty_cache()

@@ -95,16 +95,20 @@ def test_stream_extreme_and_constant_blocks(mats):
     assert np.all(sse == 0.0)  # a constant image is reconstructed exactly at every r
 
 
-def test_stream_large_stack_sampled(mats):
-    """Launch configuration of the bench (persistent grid, many chunks per CTA): 64 luma-size
-    frames, oracle on 3 sampled frames."""
-    y = synth.ar1_stack(64, 2160, 3840, 0.95, seed=4, device=DEV, batch=8)
-    sse = adct.approx_dct8x8_fused_sse(mats["T1"], y, [10]).cpu().numpy()
-    for f in (0, 31, 63):
-        _check(sse[f:f + 1], oracle.codec_sse(y[f:f + 1].cpu().numpy(), [10], t=M.T1))
-    # shard invariance: the same frames in a different stack give identical sums
-    part = adct.approx_dct8x8_fused_sse(mats["T1"], y[31:40], [10]).cpu().numpy()
-    assert np.array_equal(part, sse[31:40])
+def test_stream_config4_full_size_sampled(mats):
+    """BASELINE config 4 at full size in the bench's launch configuration: the 512-frame
+    3840x2160 luma stack and both 1920x1080 chroma stacks of bench.py (same generator and
+    seed), one call per plane; the oracle on frames 0, 255 and 511 of every plane."""
+    planes = synth.yuv420_stack(512, 2160, 3840, seed=4, device=DEV, batch=8)
+    for plane in planes:
+        sse = adct.approx_dct8x8_fused_sse(mats["T1"], plane, [10]).cpu().numpy()
+        for f in (0, 255, 511):
+            _check(sse[f:f + 1], oracle.codec_sse(plane[f:f + 1].cpu().numpy(), [10], t=M.T1))
+        # shard invariance: the same frames in a different stack give identical sums
+        part = adct.approx_dct8x8_fused_sse(mats["T1"], plane[250:260], [10]).cpu().numpy()
+        assert np.array_equal(part, sse[250:260])
+    del planes
+    torch.cuda.empty_cache()
 
 
 _VARIANT_SCRIPT = textwrap.dedent("""
