@@ -134,3 +134,10 @@ def test_status_strings():
     for s in range(8):
         assert adct.lib.adct_status_str(s)
     assert math.isfinite(adct.launch_count())
+
+
+def test_catalog_greedy_constants_match_oracle():
+    from oracle import greedy as OG
+    from paper_1808_02950_b200 import catalog
+    assert tuple(catalog.P1) == OG.P1 and tuple(catalog.P2) == OG.P2
+    assert catalog.GREEDY_FIXED_ROWS == OG.FIXED_ROWS
