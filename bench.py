@@ -418,8 +418,11 @@ def main():
     torch.cuda.synchronize(dev)
     geoms = [adct.geom_of(p) for p in planes]
     ws = torch.empty(max(adct.workspace_bytes(g, 1) for g in geoms), dtype=torch.uint8, device=dev)
-    # global per-frame, per-plane table (fp64), filled in this rank's rows only
-    table = torch.zeros((world * FRAMES, 3), dtype=torch.float64, device=dev)
+    # global per-frame, per-plane table (fp64): `local` holds this rank's rows (the others stay
+    # zero); every step it is copied into `table` and all-reduced, so each entry has exactly one
+    # non-zero contributor and the result is bit-identical to a single GPU
+    etab = parallel.ErrorTable(world * FRAMES, 3, rank * FRAMES, (rank + 1) * FRAMES, device=dev)
+    table = etab.table
     sse_planes = [torch.empty((FRAMES, 1), dtype=torch.float64, device=dev) for _ in range(3)]
     lo = rank * FRAMES
 
@@ -434,8 +437,8 @@ def main():
             adct.approx_dct8x8_fused_sse(m, p, [R], workspace=ws, sse=sse_planes[i], stream=stream)
             if k is not None and i == 0:
                 ev_luma[k][1].record(stream)
-            table[lo:lo + FRAMES, i:i + 1].copy_(sse_planes[i])
-        parallel.combine_error_table(table)
+            etab.set_local(i, sse_planes[i])
+        etab.combine()
 
     for _ in range(args.warmup):
         step()

@@ -28,7 +28,15 @@ def env_rank() -> tuple[int, int, int]:
 
 
 def init(backend: str | None = None) -> tuple[int, int, int]:
+    """Process group for torchrun ranks (NCCL over NVLink when CUDA is available).
+
+    Test hooks: ADCT_DIST_BACKEND overrides the backend; ADCT_ONE_DEVICE=1 puts every rank on
+    cuda:0 (with the gloo backend) so that the multi-rank host logic of bench.py can run on a
+    single-GPU box — the ranks' kernels never wait on each other, only host collectives do."""
     rank, local, world = env_rank()
+    if os.environ.get("ADCT_ONE_DEVICE") == "1":
+        local = 0
+    backend = backend or os.environ.get("ADCT_DIST_BACKEND") or None
     if world > 1 and not dist.is_initialized():
         if backend is None:
             backend = "nccl" if torch.cuda.is_available() else "gloo"
@@ -41,6 +49,27 @@ def init(backend: str | None = None) -> tuple[int, int, int]:
     elif torch.cuda.is_available():
         torch.cuda.set_device(local)
     return rank, local, world
+
+
+class ErrorTable:
+    """The global per-image error table [n_total, cols] (fp64) of a sharded run.
+
+    `local` holds this rank's rows [lo, hi) and zeros elsewhere; `combine()` copies it into the
+    output and all-reduces (SUM), so every entry has exactly one non-zero contributor and the
+    result is bit-identical to a single-process run however often it is combined.  (All-reducing
+    the output in place step after step would add the other ranks' stale copies.)"""
+
+    def __init__(self, n_total: int, cols: int, lo: int, hi: int, device=None):
+        self.lo, self.hi = lo, hi
+        self.local = torch.zeros((n_total, cols), dtype=torch.float64, device=device)
+        self.table = torch.zeros_like(self.local)
+
+    def set_local(self, col: int, values: torch.Tensor) -> None:
+        self.local[self.lo:self.hi, col:col + 1].copy_(values.reshape(self.hi - self.lo, 1))
+
+    def combine(self) -> torch.Tensor:
+        self.table.copy_(self.local)
+        return combine_error_table(self.table)
 
 
 def combine_error_table(local: torch.Tensor) -> torch.Tensor:

@@ -50,9 +50,16 @@ def _worker(rank, world, port, tables, q):
         local = torch.zeros_like(full)
         local[lo:hi] = full[lo:hi]                      # this rank filled only its own images
         parallel.combine_error_table(local)
+        # the bench's per-step pattern: combined again and again, the table must not drift
+        et = parallel.ErrorTable(n, full.shape[1], lo, hi)
+        for _ in range(3):
+            for c in range(full.shape[1]):
+                et.set_local(c, full[lo:hi, c])
+            tab = et.combine()
+        stable = tab.numpy().tobytes() == full.numpy().tobytes()
         t = parallel.max_over_ranks(float(rank) + 0.5)
         parallel.barrier()
-        q.put((rank, local.numpy().tobytes() == full.numpy().tobytes(), t))
+        q.put((rank, local.numpy().tobytes() == full.numpy().tobytes() and stable, t))
     finally:
         if dist.is_initialized():
             dist.destroy_process_group()
