@@ -141,3 +141,35 @@ def test_catalog_greedy_constants_match_oracle():
     from paper_1808_02950_b200 import catalog
     assert tuple(catalog.P1) == OG.P1 and tuple(catalog.P2) == OG.P2
     assert catalog.GREEDY_FIXED_ROWS == OG.FIXED_ROWS
+
+
+def test_argument_validation_next_rows():
+    """The next-row entry points reject bad arguments before any launch."""
+    L = adct.lib
+    fake = 1 << 20
+    c = (adct.ctypes.c_double * 64)(*catalog.exact_dct())
+    cp = adct.ctypes.cast(c, adct.ctypes.c_void_p)
+    ent = (adct.ctypes.c_int32 * 3)(-1, 0, 1)
+    ep = adct.ctypes.cast(ent, adct.ctypes.c_void_p)
+    dup = (adct.ctypes.c_int32 * 3)(-1, 0, 0)
+    # greedy: no entries, duplicate entries, workspace too small
+    assert L.adct_greedy_search(cp, ep, 0, None, 0, fake, 1, fake, fake, fake, 1 << 30, None) == 1
+    assert L.adct_greedy_search(cp, adct.ctypes.cast(dup, adct.ctypes.c_void_p), 3, None, 0, fake, 1, fake, fake,
+                                fake, 1 << 30, None) == 1
+    assert L.adct_greedy_search(cp, ep, 3, None, 0, fake, 1, fake, fake, fake, 16, None) == 7
+    assert L.adct_greedy_workspace_bytes(3) >= 9 * 8 * 6561
+    # JAM: block size, r range, geometry, alignment
+    g16 = adct.Geom(1, 32, 32, 1024, 32)
+    assert L.approx_dct_jam_roundtrip(8, fake, adct.U8, g16, 1, fake, adct.F32, 0, None) == 1
+    assert L.approx_dct_jam_roundtrip(16, fake, adct.U8, g16, 257, fake, adct.F32, 0, None) == 1
+    assert L.approx_dct_jam_roundtrip(32, fake, adct.U8, adct.Geom(1, 16, 32, 512, 32), 1, fake, adct.F32, 0,
+                                      None) == 1
+    assert L.approx_dct_jam_roundtrip(16, fake + 8, adct.U8, g16, 1, fake, adct.F32, 0, None) == 5
+    assert L.approx_dct_jam_roundtrip(16, fake, adct.U8, g16, 10, fake, adct.I16, 0, None) == 1  # needs ROUND
+    # round trip and SSIM
+    assert L.approx_dct8x8_roundtrip(adct.Matrix.from_int(catalog.T1).handle, fake, adct.I16, _fake(), 0, fake,
+                                     adct.I16, 2, None) == 1
+    assert L.ssim_reduce(fake, adct.U8, fake, adct.F32, _fake(), -1.0, 0, fake, fake, 1 << 30, None) == 1
+    assert L.ssim_reduce(fake, adct.U8, fake, adct.F32, _fake(), 255.0, 0, fake, fake, 8, None) == 7
+    # merit: negative counts
+    assert L.adct_merit_batch(cp, fake, fake, -1, fake, 4, fake, None) == 1
