@@ -465,7 +465,7 @@ def main():
     blocks_step_rank = FRAMES * BLOCKS_PER_FRAME
     value = world * blocks_step_rank / (ms_step * 1e-3)
 
-    # dominant kernel: the luma fused launch (fused_u8_kernel + its finalize_kernel;
+    # dominant kernel: the luma fused launch (fused_u8_wtile_kernel + its finalize_kernel;
     # 66,355,200 blocks x 64 algorithmic bytes), averaged over the timed steps
     luma_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_luma)
     luma_bytes = FRAMES * (H // 8) * (W // 8) * 64

@@ -29,7 +29,7 @@ bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& 
 
 namespace {
 
-// ADCT_DISABLE_STREAM=1 selects the register-prefetch kernels (A/B comparison and tests)
+// ADCT_DISABLE_STREAM=1 selects the generic fused kernels instead of the TMA-streamed ones (tests)
 const bool g_disable_stream = [] {
   const char* e = std::getenv("ADCT_DISABLE_STREAM");
   return e && e[0] == '1';

@@ -373,7 +373,7 @@ bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const 
 }  // namespace
 
 // The streaming path for (u8 source, integer matrix, no clip, one r); returns false when the
-// geometry or r is not covered (the caller then uses the register-prefetch kernels).
+// geometry or r is not covered (the caller then uses the generic fused kernels).
 // On success the per-image SSE is in sse[n_images] (finalize launched on st).
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
                      double* partial, cudaStream_t st, adct_status* status) {
