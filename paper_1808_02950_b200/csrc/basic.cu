@@ -9,6 +9,7 @@
 #include <mutex>
 
 #include "adct_host.h"
+#include "tma.cuh"
 
 namespace adct {
 namespace {
@@ -288,35 +289,9 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(const double* __restri
 // order and finalize_kernel averages an image's tiles in index order.
 constexpr int kSsimT = 32, kSsimIn = kSsimT + 7, kSsimNT = 256, kSsimSeg = 4;  // positions per running-sum segment
 
-template <typename OrigT, typename RecT>
-__global__ void __launch_bounds__(kSsimNT) ssim_kernel(const OrigT* __restrict__ orig, const RecT* __restrict__ rec,
-                                                       KGeom g, int32_t height, int32_t width, int32_t ntx,
-                                                       int32_t tiles, int clip, float lo, float hi, double c1,
-                                                       double c2, double* __restrict__ partial) {
-  extern __shared__ double ssm[];
-  float* sx = reinterpret_cast<float*>(ssm);                 // [39][40]
-  float* sy = sx + kSsimIn * 40;                             // [39][40]
-  double* hs = ssm + (kSsimIn * 40 * 2 + 1) / 2;             // [5][39][32]
-  __shared__ double red[kSsimNT / 32];
-  const uint32_t img = blockIdx.y;
-  const int32_t tx = (int32_t)blockIdx.x % ntx, ty = (int32_t)blockIdx.x / ntx;
-  const int32_t x0 = tx * kSsimT, y0 = ty * kSsimT;
-  const int64_t ibase = (int64_t)img * g.image_stride;
-  for (int i = threadIdx.x; i < kSsimIn * kSsimIn; i += kSsimNT) {
-    const int r = i / kSsimIn, c = i % kSsimIn;
-    const int yy = y0 + r, xx = x0 + c;
-    float a = 0.0f, b = 0.0f;
-    if (yy < height && xx < width) {
-      const int64_t off = ibase + (int64_t)yy * g.row_stride + xx;
-      a = (float)orig[off];
-      b = (float)rec[off];
-      if (clip != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
-      if (clip == ADCT_CLIP_ROUND) b = rintf(b);
-    }
-    sx[r * 40 + c] = a;
-    sy[r * 40 + c] = b;
-  }
-  __syncthreads();
+// the window SSIMs of one 32x32 tile of positions from the 39x39 samples in sx, sy
+__device__ __forceinline__ double ssim_tile_compute(const float* sx, const float* sy, double* hs, int32_t y0,
+                                                    int32_t x0, int32_t height, int32_t width, double c1, double c2) {
   // horizontal 8-sums as running sums along row segments of 8 positions
   for (int it = threadIdx.x; it < kSsimIn * (kSsimT / kSsimSeg); it += kSsimNT) {
     const int r = it / (kSsimT / kSsimSeg), c0 = (it % (kSsimT / kSsimSeg)) * kSsimSeg;
@@ -377,9 +352,108 @@ __global__ void __launch_bounds__(kSsimNT) ssim_kernel(const OrigT* __restrict__
       acc += ((2.0 * mx * my + c1) * (2.0 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2));
     }
   }
+  return acc;
+}
+
+template <typename OrigT, typename RecT>
+__global__ void __launch_bounds__(kSsimNT) ssim_kernel(const OrigT* __restrict__ orig, const RecT* __restrict__ rec,
+                                                       KGeom g, int32_t height, int32_t width, int32_t ntx,
+                                                       int32_t tiles, int clip, float lo, float hi, double c1,
+                                                       double c2, double* __restrict__ partial) {
+  extern __shared__ double ssm[];
+  float* sx = reinterpret_cast<float*>(ssm);                 // [39][40]
+  float* sy = sx + kSsimIn * 40;                             // [39][40]
+  double* hs = ssm + (kSsimIn * 40 * 2 + 1) / 2;             // [5][39][32]
+  __shared__ double red[kSsimNT / 32];
+  const uint32_t img = blockIdx.y;
+  const int32_t tx = (int32_t)blockIdx.x % ntx, ty = (int32_t)blockIdx.x / ntx;
+  const int32_t x0 = tx * kSsimT, y0 = ty * kSsimT;
+  const int64_t ibase = (int64_t)img * g.image_stride;
+  for (int i = threadIdx.x; i < kSsimIn * kSsimIn; i += kSsimNT) {
+    const int r = i / kSsimIn, c = i % kSsimIn;
+    const int yy = y0 + r, xx = x0 + c;
+    float a = 0.0f, b = 0.0f;
+    if (yy < height && xx < width) {
+      const int64_t off = ibase + (int64_t)yy * g.row_stride + xx;
+      a = (float)orig[off];
+      b = (float)rec[off];
+      if (clip != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
+      if (clip == ADCT_CLIP_ROUND) b = rintf(b);
+    }
+    sx[r * 40 + c] = a;
+    sy[r * 40 + c] = b;
+  }
+  __syncthreads();
+  const double acc = ssim_tile_compute(sx, sy, hs, y0, x0, height, width, c1, c2);
   const double tot = block_sum<kSsimNT>(acc, red);
   if (threadIdx.x == 0) partial[(int64_t)img * tiles + blockIdx.x] = tot;
 }
+
+// Persistent variant for u8 originals and fp32 reconstructions: each CTA walks its tiles with a
+// 2-slot TMA ring (the 48x39 u8 and 40x39 fp32 boxes of the next tile land while the current one
+// is computed), so the global-load latency that bounds ssim_kernel is hidden.
+constexpr int kSsimBoxO = 48, kSsimBoxR = 40;  // box widths: 16-byte multiples >= 39
+constexpr uint32_t kSsimStageO = kSsimIn * kSsimBoxO, kSsimStageR = kSsimIn * kSsimBoxR * 4;
+constexpr uint32_t kSsimStage = ((kSsimStageO + 127) / 128 * 128 + kSsimStageR + 127) / 128 * 128;  // TMA
+// destinations are 128-byte aligned
+
+__global__ void __launch_bounds__(kSsimNT) ssim_tma_kernel(const __grid_constant__ CUtensorMap to,
+                                                           const __grid_constant__ CUtensorMap tr, int32_t height,
+                                                           int32_t width, int32_t ntx, int32_t tiles,
+                                                           int64_t n_tiles, int clip, float lo, float hi, double c1,
+                                                           double c2, double* __restrict__ partial) {
+  extern __shared__ __align__(128) uint8_t sraw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>(((uintptr_t)sraw + 127) & ~(uintptr_t)127);
+  uint8_t* stage = base;                                        // 2 x kSsimStage
+  float* sx = reinterpret_cast<float*>(base + 2 * kSsimStage);  // [39][40]
+  float* sy = sx + kSsimIn * 40;
+  double* hs = reinterpret_cast<double*>(sy + kSsimIn * 40);   // [5][39][32]
+  uint64_t* full = reinterpret_cast<uint64_t*>(hs + 5 * kSsimIn * kSsimT);
+  __shared__ double red[kSsimNT / 32];
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t, int slot) {
+    const int32_t img = (int32_t)(t / tiles), tl = (int32_t)(t % tiles);
+    const int32_t x0 = (tl % ntx) * kSsimT, y0 = (tl / ntx) * kSsimT;
+    uint8_t* st = stage + slot * kSsimStage;
+    mbar_arrive_expect_tx(&full[slot], kSsimStageO + kSsimStageR);
+    tma_load_3d(smem_u32(st), &to, x0, y0, img, smem_u32(&full[slot]));
+    tma_load_3d(smem_u32(st + (kSsimStageO + 127) / 128 * 128), &tr, x0, y0, img, smem_u32(&full[slot]));
+  };
+  if (threadIdx.x == 0 && (int64_t)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+  uint32_t k = 0;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
+    const int slot = (int)(k & 1u);
+    mbar_wait(&full[slot], (k >> 1) & 1u);
+    const uint8_t* so = stage + slot * kSsimStage;
+    const float* sr = reinterpret_cast<const float*>(so + (kSsimStageO + 127) / 128 * 128);
+    for (int i = threadIdx.x; i < kSsimIn * kSsimIn; i += kSsimNT) {
+      const int r = i / kSsimIn, c = i % kSsimIn;
+      float b = sr[r * kSsimBoxR + c];
+      if (clip != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
+      if (clip == ADCT_CLIP_ROUND) b = rintf(b);
+      sx[r * 40 + c] = (float)so[r * kSsimBoxO + c];
+      sy[r * 40 + c] = b;
+    }
+    __syncthreads();  // the slot is consumed: prefetch the CTA's next tile into the other slot
+    if (threadIdx.x == 0 && t + gridDim.x < n_tiles) {
+      fence_proxy_async();
+      issue(t + gridDim.x, slot ^ 1);
+    }
+    const int32_t img = (int32_t)(t / tiles), tl = (int32_t)(t % tiles);
+    const double acc =
+        ssim_tile_compute(sx, sy, hs, (tl / ntx) * kSsimT, (tl % ntx) * kSsimT, height, width, c1, c2);
+    const double tot = block_sum<kSsimNT>(acc, red);  // also orders this tile's reads before the next
+    if (threadIdx.x == 0) partial[(int64_t)img * tiles + tl] = tot;
+  }
+}
+
+constexpr size_t kSsimTmaSmem = 128 + 2 * (size_t)kSsimStage + (size_t)kSsimIn * 40 * 4 * 2 +
+                                (size_t)5 * kSsimIn * kSsimT * 8 + 16;
 
 constexpr size_t kSsimSmem = (size_t)(kSsimIn * 40 * 2 + 1) / 2 * 8 + (size_t)5 * kSsimIn * kSsimT * 8;
 
@@ -602,6 +676,41 @@ adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
     cudaFuncSetAttribute(ssim_kernel<int16_t, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
     cudaFuncSetAttribute(ssim_kernel<int16_t, int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
   });
+  if (orig_t == ADCT_U8 && recon_t == ADCT_F32 && g.row_stride % 16 == 0 &&
+      (g.n_images == 1 || g.image_stride % 16 == 0) && aligned(orig, 16) && aligned(recon, 16)) {
+    auto enc = tmap_encoder();
+    CUtensorMap to, tr;
+    const cuuint64_t dims[3] = {(cuuint64_t)g.width, (cuuint64_t)g.height, (cuuint64_t)g.n_images};
+    const int64_t istr = g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride;
+    const cuuint64_t so[2] = {(cuuint64_t)g.row_stride, (cuuint64_t)istr};
+    const cuuint64_t sr[2] = {(cuuint64_t)g.row_stride * 4, (cuuint64_t)istr * 4};
+    const cuuint32_t bo[3] = {(cuuint32_t)kSsimBoxO, (cuuint32_t)kSsimIn, 1}, br[3] = {(cuuint32_t)kSsimBoxR, (cuuint32_t)kSsimIn, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (enc &&
+        enc(&to, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(orig), dims, so, bo, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+            CUDA_SUCCESS &&
+        enc(&tr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(recon), dims, sr, br, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      static std::once_flag once_tma;
+      std::call_once(once_tma, [] {
+        cudaFuncSetAttribute(ssim_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimTmaSmem);
+      });
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t n_tiles = (int64_t)tiles * g.n_images;
+      const int64_t cap = (int64_t)sms * 2;
+      ssim_tma_kernel<<<(unsigned)(n_tiles < cap ? n_tiles : cap), kSsimNT, kSsimTmaSmem, st>>>(
+          to, tr, g.height, g.width, ntx, tiles, n_tiles, (int)clip, lo, hi, c1, c2, partial);
+      count_launch();
+      if (adct_status e = launch_status()) return e;
+      const double nwin = (double)(g.height - 7) * (double)(g.width - 7);
+      launch_finalize_scaled(partial, tiles, g.n_images, 1.0 / nwin, ssim, st);
+      return launch_status();
+    }
+  }
   const dim3 grid((unsigned)tiles, (unsigned)g.n_images);
 #define ADCT_SSIM(OT, RT)                                                                                      \
   ssim_kernel<OT, RT><<<grid, kSsimNT, kSsimSmem, st>>>((const OT*)orig, (const RT*)recon, kg, g.height, g.width, \

@@ -389,6 +389,17 @@ def test_ssim_reduce_matches_oracle(shape, rtype):
         assert np.allclose(got, ref, rtol=1e-9, atol=1e-12), (got, ref)
 
 
+def test_ssim_tma_path_many_tiles_per_cta():
+    """u8 originals with fp32 reconstructions and 16-byte strides take the persistent TMA kernel;
+    enough images that every CTA walks several tiles through both ring slots."""
+    x = images("ar1", 40, 256, 272, seed=9)
+    r = (x.float() + torch.from_numpy(np.random.default_rng(1).normal(0, 9, size=x.shape).astype(np.float32)))
+    for clip in (adct.CLIP_NONE, adct.CLIP):
+        got = adct.ssim_reduce(x.to(DEV), r.to(DEV), clip=clip).cpu().numpy()
+        ref = OS.ssim(x.numpy(), r.numpy(), clip=clip)
+        assert np.allclose(got, ref, rtol=1e-9, atol=1e-12)
+
+
 def test_ssim_identical_is_one_and_pipeline(mats):
     """SSIM(x, x) = 1; and the C1-shaped pipeline fwd -> retain r -> inv (fused round trip) ->
     SSIM against the oracle composition, for T1 and the DCT, at the paper's r = 3 and 14
