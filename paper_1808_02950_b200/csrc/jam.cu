@@ -8,12 +8,12 @@
 // first and the butterfly last.  All intermediates are integers < 2^24 for |x| <= 7281, so the
 // forward is exact in fp32.
 //
-// One CTA of 256 threads owns 256/N blocks.  Pass 1: thread (block b, row i) loads row i,
+// One CTA of 256 threads owns 256/N blocks per iteration.  Pass 1: thread (block b, row i) loads row i,
 // applies T(N) (row transform) and stores it to shared memory.  Pass 2: thread (b, column k)
 // applies T(N) down the column, the weights W_kl = keep_kl / (d_k d_l), d = diag(T T^T)
 // (P:L2742-2770), and T(N)^T back up the column.  Pass 3: thread (b, i) applies T(N)^T to its row
-// and writes the reconstruction.  An odd row pitch (N + 1) keeps the shared-memory passes
-// conflict-free.
+// and writes the reconstruction.  A row pitch of an odd number of 16-byte units (N + 4) keeps
+// the 128-bit row passes and the scalar column pass conflict-free.
 #include <cstring>
 #include <mutex>
 
@@ -23,6 +23,14 @@ namespace adct {
 namespace {
 
 constexpr int kJamNT = 256;
+// Resident CTAs per SM the register budget is cut for (B200 sweep, int16 r = N^2: T(16) 5 -> 48
+// registers, T(32) 3 -> 80, both spill-free; tighter budgets spill and run up to 1.6x slower)
+#ifndef ADCT_JAM_MINB16
+#define ADCT_JAM_MINB16 5
+#endif
+#ifndef ADCT_JAM_MINB32
+#define ADCT_JAM_MINB32 3
+#endif
 
 // y = T(N) x
 template <int N>
@@ -75,27 +83,38 @@ struct JamW {
   float w[N * N];  // keep_kl / (d_k d_l)
 };
 
-// N samples of one row as fp32 (16-byte vector loads; rows are 16-byte aligned).  Conversions
-// avoid the quarter-rate XU pipe (I2F/F2I): a u8 sample is placed in the mantissa of 2^23 by one
-// PRMT and the 2^23 removed by an FADD; an int16 sample is sign-extended (PRMT / SHF) and
-// converted by I2FP on the ALU pipe; results are rounded with the 1.5*2^23 trick.
+// One row of N samples, raw (16-byte vector loads; rows are 16-byte aligned), then as fp32.
+// Conversions avoid the quarter-rate XU pipe (I2F/F2I): a u8 sample is placed in the mantissa of
+// 2^23 by one PRMT and the 2^23 removed by an FADD; an int16 sample is sign-extended (PRMT / SHF)
+// and converted by I2FP on the ALU pipe; results are rounded with the 1.5*2^23 trick.
+template <int N, typename SrcT>
+struct RawRow {
+  static constexpr int NV = N * (int)sizeof(SrcT) / 16;
+  uint4 v[NV];
+  __device__ __forceinline__ void load(const SrcT* p) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) v[c] = __ldg(reinterpret_cast<const uint4*>(p) + c);
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) v[c] = make_uint4(0u, 0u, 0u, 0u);
+  }
+};
 template <int N>
-__device__ __forceinline__ void load_row(const uint8_t* p, float* x) {
+__device__ __forceinline__ void to_float(const RawRow<N, uint8_t>& r, float* x) {
 #pragma unroll
   for (int c = 0; c < N / 16; ++c) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + c);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    const uint32_t w[4] = {r.v[c].x, r.v[c].y, r.v[c].z, r.v[c].w};
 #pragma unroll
     for (int q = 0; q < 16; ++q)
       x[c * 16 + q] = __uint_as_float(__byte_perm(w[q >> 2], 0x4B000000u, 0x7440u | (uint32_t)(q & 3))) - 8388608.0f;
   }
 }
 template <int N>
-__device__ __forceinline__ void load_row(const int16_t* p, float* x) {
+__device__ __forceinline__ void to_float(const RawRow<N, int16_t>& r, float* x) {
 #pragma unroll
   for (int c = 0; c < N / 8; ++c) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + c);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    const uint32_t w[4] = {r.v[c].x, r.v[c].y, r.v[c].z, r.v[c].w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       x[c * 8 + 2 * q] = (float)(int32_t)__byte_perm(w[q], 0u, 0x9910u);  // sign-extended low half
@@ -107,12 +126,32 @@ __device__ __forceinline__ void load_row(const int16_t* p, float* x) {
 // low 16 (or 8) bits of 1.5*2^23 + v: v rounded half to even, two's complement
 __device__ __forceinline__ uint32_t rbits(float v) { return __float_as_uint(v + 12582912.0f); }
 
-template <int N>
+// v rounded half to even as an int32 (|v| < 2^22: the reconstruction is an orthogonal projection
+// of the block, so |v| <= ||x||_2 <= 32768 * N)
+__device__ __forceinline__ int32_t rint_s32(float v) { return (int32_t)(rbits(v) - 0x4B400000u); }
+// (sat_s16(hi) << 16) | sat_s16(lo): one I2IP for two samples
+__device__ __forceinline__ uint32_t pack_sat_s16(int32_t hi, int32_t lo) {
+  uint32_t d;
+  asm("cvt.pack.sat.s16.s32 %0, %1, %2;" : "=r"(d) : "r"(hi), "r"(lo));
+  return d;
+}
+
+// SAT16: x is unclipped and the int16 range is the clip range (int16 source)
+template <int N, bool SAT16>
 __device__ __forceinline__ void store_row_any(void* recon, int64_t off, int out_t, const float* x) {
   if (out_t == ADCT_F32) {
     float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(recon) + off);
 #pragma unroll
     for (int c = 0; c < N / 4; ++c) o[c] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+  } else if (out_t == ADCT_I16 && SAT16) {  // rounded here, saturated by the pack (CLIP_ROUND)
+    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<int16_t*>(recon) + off);
+#pragma unroll
+    for (int c = 0; c < N / 8; ++c) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = pack_sat_s16(rint_s32(x[8 * c + 2 * q + 1]), rint_s32(x[8 * c + 2 * q]));
+      o[c] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
   } else if (out_t == ADCT_I16) {  // x already rounded and saturated (CLIP_ROUND)
     uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<int16_t*>(recon) + off);
 #pragma unroll
@@ -138,41 +177,54 @@ __device__ __forceinline__ void store_row_any(void* recon, int64_t off, int out_
   }
 }
 
+template <int N>
+__device__ __forceinline__ int64_t jam_row_offset(uint32_t b, int i, const KGeom& g, FastDiv dnbi, FastDiv dbw) {
+  const uint32_t img = fdiv(b, dnbi);
+  const uint32_t q = b - img * g.nbi;
+  const uint32_t by = fdiv(q, dbw);
+  const uint32_t bx = q - by * g.bw;
+  return (int64_t)img * g.image_stride + ((int64_t)by * N + i) * g.row_stride + (int64_t)bx * N;
+}
+
+// Persistent (grid = SMs x resident CTAs).  The next iteration's row is loaded into registers
+// right after pass 1 consumes the current one, so its HBM latency overlaps passes 2-3.  Two
+// barriers per iteration: pass 3 and the next pass 1 touch only the thread's own row.
 template <int N, typename SrcT>
-__global__ void __launch_bounds__(kJamNT) jam_roundtrip_kernel(const SrcT* __restrict__ src, KGeom g, JamW<N> wt,
+__global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_MINB32) jam_roundtrip_kernel(const SrcT* __restrict__ src, KGeom g, JamW<N> wt,
                                                                uint32_t nblocks, FastDiv dnbi, FastDiv dbw,
                                                                int out_t, int clip, float lo, float hi,
                                                                void* __restrict__ recon) {
   constexpr int BPC = kJamNT / N;  // blocks per CTA
-  constexpr int P = N + 1;         // odd row pitch: row writes and column reads are conflict-free
-  __shared__ float sm[BPC * N * P];
-  __shared__ float sw[N * N];  // weights: lanes read different columns (a constant-bank read would serialise)
-  for (int t = threadIdx.x; t < N * N; t += kJamNT) sw[t] = wt.w[t];
-  __syncthreads();
+  constexpr bool kSat16 = sizeof(SrcT) == 2;
+  // row pitch N + 4 floats = an odd number of 16-byte units: 128-bit row accesses (8 lanes per
+  // phase, rows i..i+7) and scalar column accesses (consecutive columns) are both conflict-free
+  constexpr int P = N + 4;
+  __shared__ __align__(16) float sm[BPC * N * P];
+  __shared__ __align__(16) float sw[N * P];  // weights transposed, sw[l][k]: column l reads its k's as float4
+  for (int t = threadIdx.x; t < N * N; t += kJamNT) sw[(t % N) * P + t / N] = wt.w[t];
   const int bl = threadIdx.x / N, i = threadIdx.x % N;  // thread = (block, row i) = (block, column i)
-  for (uint32_t b0 = blockIdx.x * BPC; b0 < nblocks; b0 += gridDim.x * BPC) {
-    const uint32_t b = b0 + bl;
-    const bool valid = b < nblocks;
-    int64_t off = 0;
-    if (valid) {
-      const uint32_t img = fdiv(b, dnbi);
-      const uint32_t q = b - img * g.nbi;
-      const uint32_t by = fdiv(q, dbw);
-      const uint32_t bx = q - by * g.bw;
-      off = (int64_t)img * g.image_stride + ((int64_t)by * N + i) * g.row_stride + (int64_t)bx * N;
-    }
-    float* row = sm + (bl * N + i) * P;
+  const uint32_t stride = gridDim.x * BPC;
+  float* row = sm + (bl * N + i) * P;
+  uint32_t b = blockIdx.x * BPC + bl;
+  bool valid = b < nblocks;
+  int64_t off = valid ? jam_row_offset<N>(b, i, g, dnbi, dbw) : 0;
+  RawRow<N, SrcT> raw;
+  if (valid) raw.load(src + off);
+  else raw.zero();
+  __syncthreads();
+  for (uint32_t b0 = blockIdx.x * BPC; b0 < nblocks; b0 += stride) {
     {  // pass 1: row i of block bl, forward
       float x[N], y[N];
-      if (valid) load_row<N>(src + off, x);
-      else {
-#pragma unroll
-        for (int j = 0; j < N; ++j) x[j] = 0.0f;
-      }
+      to_float<N>(raw, x);
       Jam<N>::fwd(x, y);
 #pragma unroll
-      for (int j = 0; j < N; ++j) row[j] = y[j];
+      for (int j = 0; j < N; j += 4) *reinterpret_cast<float4*>(row + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
     }
+    const uint32_t bn = b + stride;  // prefetch the next iteration's row
+    const bool vn = bn < nblocks;
+    const int64_t offn = vn ? jam_row_offset<N>(bn, i, g, dnbi, dbw) : 0;
+    if (vn) raw.load(src + offn);
+    else raw.zero();
     __syncthreads();
     {  // pass 2: column i (frequency l = i) of block bl: forward, weights, inverse
       float c[N], y[N];
@@ -180,7 +232,13 @@ __global__ void __launch_bounds__(kJamNT) jam_roundtrip_kernel(const SrcT* __res
       for (int k = 0; k < N; ++k) c[k] = sm[(bl * N + k) * P + i];
       Jam<N>::fwd(c, y);
 #pragma unroll
-      for (int k = 0; k < N; ++k) y[k] *= sw[k * N + i];
+      for (int k = 0; k < N; k += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(sw + i * P + k);
+        y[k] *= w4.x;
+        y[k + 1] *= w4.y;
+        y[k + 2] *= w4.z;
+        y[k + 3] *= w4.w;
+      }
       Jam<N>::inv(y, c);
 #pragma unroll
       for (int k = 0; k < N; ++k) sm[(bl * N + k) * P + i] = c[k];
@@ -189,9 +247,17 @@ __global__ void __launch_bounds__(kJamNT) jam_roundtrip_kernel(const SrcT* __res
     {  // pass 3: row i, inverse, store
       float z[N], x[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) z[j] = row[j];
+      for (int j = 0; j < N; j += 4) {
+        const float4 r4 = *reinterpret_cast<const float4*>(row + j);
+        z[j] = r4.x;
+        z[j + 1] = r4.y;
+        z[j + 2] = r4.z;
+        z[j + 3] = r4.w;
+      }
       Jam<N>::inv(z, x);
-      if (valid) {
+      if (valid && kSat16 && out_t == ADCT_I16) {  // int16 -> int16: the saturating pack is the clip
+        store_row_any<N, true>(recon, off, out_t, x);
+      } else if (valid) {
 #pragma unroll
         for (int j = 0; j < N; ++j) {
           float v = x[j];
@@ -199,10 +265,12 @@ __global__ void __launch_bounds__(kJamNT) jam_roundtrip_kernel(const SrcT* __res
           if (clip == ADCT_CLIP_ROUND && out_t == ADCT_F32) v = rintf(v);  // integer stores round themselves
           x[j] = v;
         }
-        store_row_any<N>(recon, off, out_t, x);
+        store_row_any<N, false>(recon, off, out_t, x);
       }
     }
-    __syncthreads();
+    b = bn;
+    valid = vn;
+    off = offn;
   }
 }
 
@@ -246,10 +314,14 @@ adct_status launch_jam(const void* src, const adct_geom& g, int32_t r, void* rec
   const uint32_t nb = (uint32_t)(g.n_images * kg.nbi);
   if (nb == 0) return ADCT_OK;
   constexpr int BPC = kJamNT / N;
-  int dev = 0, sms = 148;
+  int dev = 0, sms = 148, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t need = ((int64_t)nb + BPC - 1) / BPC, cap = (int64_t)sms * 8;
+  // one wave of resident CTAs: a grid beyond it would leave a second, partly occupied wave
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jam_roundtrip_kernel<N, SrcT>, kJamNT, 0) != cudaSuccess ||
+      occ < 1)
+    occ = 1;
+  const int64_t need = ((int64_t)nb + BPC - 1) / BPC, cap = (int64_t)sms * occ;
   const unsigned grid = (unsigned)(need < cap ? need : cap);
   jam_roundtrip_kernel<N, SrcT><<<grid, kJamNT, 0, st>>>((const SrcT*)src, kg, wt, nb, make_fastdiv(kg.nbi),
                                                          make_fastdiv(kg.bw), (int)recon_t, (int)clip, lo, hi, recon);
