@@ -7,9 +7,9 @@
 // sized in multiples of the SM count.
 #include <cmath>
 #include <mutex>
+#include <type_traits>
 
 #include "adct_host.h"
-#include "tma.cuh"
 
 namespace adct {
 namespace {
@@ -283,185 +283,157 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(const double* __restri
 }
 
 // ---- SSIM (reading A18: 8x8 uniform windows, K1 = 0.01, K2 = 0.03, L = peak) -------------------
-// One CTA per 32x32 tile of window positions: the 39x39 samples of both images are staged in
-// shared memory, horizontal 8-sums of x, y, x^2, y^2, xy are formed per row, then vertical
-// 8-sums per position, all in fp64; per-CTA sums of the window SSIMs are reduced in a fixed
-// order and finalize_kernel averages an image's tiles in index order.
-constexpr int kSsimT = 32, kSsimIn = kSsimT + 7, kSsimNT = 256, kSsimSeg = 4;  // positions per running-sum segment
+// One warp per (image, band of kSsTY window rows, strip of 25 window columns): lane l owns input
+// column x0 + l and walks down the band's kSsTY + 7 input rows with vertical running 8-sums of
+// x, y, x^2, y^2, xy held in registers (the previous 8 rows stay in a register ring, so each
+// row is loaded once); the 8-wide horizontal window sums are three shuffle-add steps across
+// lanes l..l+7, so lanes 0..24 each own one window per row.  No shared memory, no barriers;
+// rows are prefetched one 8-row group ahead.  Sums of a u8 original are exact in fp32 (integers
+// < 2^24); the rest is fp64.  The window SSIM is evaluated on sums scaled by 64^2:
+//   SSIM = (2P + 4096 C1)(128 S_xy - 2P + 4096 C2) / ((Q + 4096 C1)(64 (S_xx + S_yy) - Q + 4096 C2)),
+//   P = S_x S_y, Q = S_x^2 + S_y^2,
+// the definition's mu = S/64, sigma^2 = S_xx/64 - mu^2, sigma_xy = S_xy/64 - mu_x mu_y
+// multiplied through.  Each warp's windows are summed in a fixed shuffle tree and
+// finalize_kernel adds an image's warps in index order.
+constexpr int kSsOut = 25, kSsTY = 64, kSsNT = 32;  // one warp per CTA: the control flow is
+// provably warp-uniform (blockIdx only), so the shuffles need no re-convergence code
 
-// the window SSIMs of one 32x32 tile of positions from the 39x39 samples in sx, sy
-__device__ __forceinline__ double ssim_tile_compute(const float* sx, const float* sy, double* hs, int32_t y0,
-                                                    int32_t x0, int32_t height, int32_t width, double c1, double c2) {
-  // horizontal 8-sums as running sums along row segments of 8 positions
-  for (int it = threadIdx.x; it < kSsimIn * (kSsimT / kSsimSeg); it += kSsimNT) {
-    const int r = it / (kSsimT / kSsimSeg), c0 = (it % (kSsimT / kSsimSeg)) * kSsimSeg;
-    const float* px = sx + r * 40;
-    const float* py = sy + r * 40;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double a = px[c0 + k], b = py[c0 + k];
-      s0 += a;
-      s1 += b;
-      s2 = fma(a, a, s2);
-      s3 = fma(b, b, s3);
-      s4 = fma(a, b, s4);
-    }
-#pragma unroll
-    for (int c = c0; c < c0 + kSsimSeg; ++c) {
-      if (c > c0) {  // slide the window by one: add sample c+7, drop sample c-1
-        const double a = px[c + 7], b = py[c + 7], a0 = px[c - 1], b0 = py[c - 1];
-        s0 += a - a0;
-        s1 += b - b0;
-        s2 += fma(a, a, -a0 * a0);
-        s3 += fma(b, b, -b0 * b0);
-        s4 += fma(a, b, -a0 * b0);
-      }
-      const int i = r * kSsimT + c;
-      hs[0 * kSsimIn * kSsimT + i] = s0;
-      hs[1 * kSsimIn * kSsimT + i] = s1;
-      hs[2 * kSsimIn * kSsimT + i] = s2;
-      hs[3 * kSsimIn * kSsimT + i] = s3;
-      hs[4 * kSsimIn * kSsimT + i] = s4;
-    }
-  }
-  __syncthreads();
-  // vertical 8-sums as running sums down column segments of 8 positions, then the window SSIM
-  double acc = 0.0;
-  for (int it = threadIdx.x; it < kSsimT * (kSsimT / kSsimSeg); it += kSsimNT) {
-    const int c = it % kSsimT, r0 = (it / kSsimT) * kSsimSeg;
-    double v[5];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) t += hs[q * kSsimIn * kSsimT + (r0 + k) * kSsimT + c];
-      v[q] = t;
-    }
-#pragma unroll
-    for (int r = r0; r < r0 + kSsimSeg; ++r) {
-      if (r > r0) {
-#pragma unroll
-        for (int q = 0; q < 5; ++q)
-          v[q] += hs[q * kSsimIn * kSsimT + (r + 7) * kSsimT + c] - hs[q * kSsimIn * kSsimT + (r - 1) * kSsimT + c];
-      }
-      if (y0 + r + 8 > height || x0 + c + 8 > width) continue;
-      const double mx = v[0] * (1.0 / 64.0), my = v[1] * (1.0 / 64.0);
-      const double vx = v[2] * (1.0 / 64.0) - mx * mx, vy = v[3] * (1.0 / 64.0) - my * my;
-      const double cxy = v[4] * (1.0 / 64.0) - mx * my;
-      acc += ((2.0 * mx * my + c1) * (2.0 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2));
-    }
-  }
-  return acc;
+// Sums of x and x^2: fp32 for a u8 original (integers < 2^24: exact), fp64 for int16.
+template <typename OrigT>
+using SsAcc = std::conditional_t<sizeof(OrigT) == 1, float, double>;
+
+template <typename T>
+__device__ __forceinline__ T win8(T v) {  // lane l: v_l + ... + v_{l+7} in a fixed order
+  v += __shfl_down_sync(0xffffffffu, v, 1);
+  v += __shfl_down_sync(0xffffffffu, v, 2);
+  v += __shfl_down_sync(0xffffffffu, v, 4);
+  return v;
+}
+
+// n / d for d > 0 (the SSIM denominator is >= 4096^2 C1 C2): MUFU reciprocal seed and two
+// Newton steps, then one product -- within 2 ulp, no slow-path branch of the IEEE division
+__device__ __forceinline__ double ss_div(double n, double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  return n * r;
 }
 
 template <typename OrigT, typename RecT>
-__global__ void __launch_bounds__(kSsimNT) ssim_kernel(const OrigT* __restrict__ orig, const RecT* __restrict__ rec,
-                                                       KGeom g, int32_t height, int32_t width, int32_t ntx,
-                                                       int32_t tiles, int clip, float lo, float hi, double c1,
-                                                       double c2, double* __restrict__ partial) {
-  extern __shared__ double ssm[];
-  float* sx = reinterpret_cast<float*>(ssm);                 // [39][40]
-  float* sy = sx + kSsimIn * 40;                             // [39][40]
-  double* hs = ssm + (kSsimIn * 40 * 2 + 1) / 2;             // [5][39][32]
-  __shared__ double red[kSsimNT / 32];
-  const uint32_t img = blockIdx.y;
-  const int32_t tx = (int32_t)blockIdx.x % ntx, ty = (int32_t)blockIdx.x / ntx;
-  const int32_t x0 = tx * kSsimT, y0 = ty * kSsimT;
-  const int64_t ibase = (int64_t)img * g.image_stride;
-  for (int i = threadIdx.x; i < kSsimIn * kSsimIn; i += kSsimNT) {
-    const int r = i / kSsimIn, c = i % kSsimIn;
-    const int yy = y0 + r, xx = x0 + c;
-    float a = 0.0f, b = 0.0f;
-    if (yy < height && xx < width) {
-      const int64_t off = ibase + (int64_t)yy * g.row_stride + xx;
-      a = (float)orig[off];
-      b = (float)rec[off];
-      if (clip != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
-      if (clip == ADCT_CLIP_ROUND) b = rintf(b);
-    }
-    sx[r * 40 + c] = a;
-    sy[r * 40 + c] = b;
+struct SsGroup {  // one lane's raw samples of 8 consecutive rows (converted when used, so the
+  OrigT a[8];     // loads of the prefetched group have a whole group of work to land)
+  RecT b[8];
+};
+
+template <typename Acc>
+struct SsState {
+  Acc A, AA;          // vertical 8-sums of x, x^2 (the lane's column)
+  double B, BB, AB;   // ... of y, y^2, xy
+  double acc;         // the lane's window SSIMs
+};
+
+template <typename OrigT, typename RecT>
+__device__ __forceinline__ void ss_load(SsGroup<OrigT, RecT>& gr, const OrigT* po, const RecT* pr, int64_t rs, int r0,
+                                        int nin, bool col_ok) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const bool ok = col_ok && r0 + k < nin;
+    gr.a[k] = ok ? __ldg(po + k * rs) : (OrigT)0;
+    gr.b[k] = ok ? __ldg(pr + k * rs) : (RecT)0;
   }
-  __syncthreads();
-  const double acc = ssim_tile_compute(sx, sy, hs, y0, x0, height, width, c1, c2);
-  const double tot = block_sum<kSsimNT>(acc, red);
-  if (threadIdx.x == 0) partial[(int64_t)img * tiles + blockIdx.x] = tot;
 }
 
-// Persistent variant for u8 originals and fp32 reconstructions: each CTA walks its tiles with a
-// 2-slot TMA ring (the 48x39 u8 and 40x39 fp32 boxes of the next tile land while the current one
-// is computed), so the global-load latency that bounds ssim_kernel is hidden.
-constexpr int kSsimBoxO = 48, kSsimBoxR = 40;  // box widths: 16-byte multiples >= 39
-constexpr uint32_t kSsimStageO = kSsimIn * kSsimBoxO, kSsimStageR = kSsimIn * kSsimBoxR * 4;
-constexpr uint32_t kSsimStage = ((kSsimStageO + 127) / 128 * 128 + kSsimStageR + 127) / 128 * 128;  // TMA
-// destinations are 128-byte aligned
-
-__global__ void __launch_bounds__(kSsimNT) ssim_tma_kernel(const __grid_constant__ CUtensorMap to,
-                                                           const __grid_constant__ CUtensorMap tr, int32_t height,
-                                                           int32_t width, int32_t ntx, int32_t tiles,
-                                                           int64_t n_tiles, int clip, float lo, float hi, double c1,
-                                                           double c2, double* __restrict__ partial) {
-  extern __shared__ __align__(128) uint8_t sraw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>(((uintptr_t)sraw + 127) & ~(uintptr_t)127);
-  uint8_t* stage = base;                                        // 2 x kSsimStage
-  float* sx = reinterpret_cast<float*>(base + 2 * kSsimStage);  // [39][40]
-  float* sy = sx + kSsimIn * 40;
-  double* hs = reinterpret_cast<double*>(sy + kSsimIn * 40);   // [5][39][32]
-  uint64_t* full = reinterpret_cast<uint64_t*>(hs + 5 * kSsimIn * kSsimT);
-  __shared__ double red[kSsimNT / 32];
-  if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int64_t t, int slot) {
-    const int32_t img = (int32_t)(t / tiles), tl = (int32_t)(t % tiles);
-    const int32_t x0 = (tl % ntx) * kSsimT, y0 = (tl / ntx) * kSsimT;
-    uint8_t* st = stage + slot * kSsimStage;
-    mbar_arrive_expect_tx(&full[slot], kSsimStageO + kSsimStageR);
-    tma_load_3d(smem_u32(st), &to, x0, y0, img, smem_u32(&full[slot]));
-    tma_load_3d(smem_u32(st + (kSsimStageO + 127) / 128 * 128), &tr, x0, y0, img, smem_u32(&full[slot]));
+// rows 8 gi .. 8 gi + 7: add row r, drop row r - 8 (the previous group's slot), and for r >= 7
+// evaluate the windows whose top row is r - 7.  Padding rows / columns are 0 before and after
+// the clip (they only reach windows that are not counted).
+template <typename Acc, typename OrigT, typename RecT>
+__device__ __forceinline__ void ss_group(SsState<Acc>& s, const SsGroup<OrigT, RecT>& cur,
+                                         const SsGroup<OrigT, RecT>& prev, int gi, int nout, bool win_ok, int clip,
+                                         float lo, float hi, double c1s, double c2s) {
+  auto y_of = [&](RecT v) {
+    float b = (float)v;
+    if (clip != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
+    if (clip == ADCT_CLIP_ROUND) b = rintf(b);
+    return (double)b;
   };
-  if (threadIdx.x == 0 && (int64_t)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
-  uint32_t k = 0;
-  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++k) {
-    const int slot = (int)(k & 1u);
-    mbar_wait(&full[slot], (k >> 1) & 1u);
-    const uint8_t* so = stage + slot * kSsimStage;
-    const float* sr = reinterpret_cast<const float*>(so + (kSsimStageO + 127) / 128 * 128);
-    for (int i = threadIdx.x; i < kSsimIn * kSsimIn; i += kSsimNT) {
-      const int r = i / kSsimIn, c = i % kSsimIn;
-      float b = sr[r * kSsimBoxR + c];
-      if (clip != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
-      if (clip == ADCT_CLIP_ROUND) b = rintf(b);
-      sx[r * 40 + c] = (float)so[r * kSsimBoxO + c];
-      sy[r * 40 + c] = b;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const Acc an = (Acc)cur.a[k], ao = (Acc)prev.a[k];
+    const double bn = y_of(cur.b[k]), bo = y_of(prev.b[k]);
+    s.A += an - ao;
+    s.AA += an * an - ao * ao;
+    s.B += bn - bo;
+    s.BB = fma(bn, bn, s.BB);
+    s.BB = fma(-bo, bo, s.BB);
+    s.AB = fma((double)an, bn, s.AB);
+    s.AB = fma(-(double)ao, bo, s.AB);
+    // every lane shuffles (converged); only windows inside the band and the image count
+    const double sa = (double)win8(s.A), saa = (double)win8(s.AA);
+    const double sb = win8(s.B), sbb = win8(s.BB), sab = win8(s.AB);
+    const int orow = gi * 8 + k - 7;
+    if (win_ok && orow >= 0 && orow < nout) {
+      const double p = sa * sb, qq = fma(sa, sa, sb * sb);
+      const double num = fma(2.0, p, c1s) * (fma(128.0, sab, c2s) - 2.0 * p);
+      const double den = (qq + c1s) * (fma(64.0, saa + sbb, c2s) - qq);
+      s.acc += ss_div(num, den);
     }
-    __syncthreads();  // the slot is consumed: prefetch the CTA's next tile into the other slot
-    if (threadIdx.x == 0 && t + gridDim.x < n_tiles) {
-      fence_proxy_async();
-      issue(t + gridDim.x, slot ^ 1);
-    }
-    const int32_t img = (int32_t)(t / tiles), tl = (int32_t)(t % tiles);
-    const double acc =
-        ssim_tile_compute(sx, sy, hs, (tl / ntx) * kSsimT, (tl % ntx) * kSsimT, height, width, c1, c2);
-    const double tot = block_sum<kSsimNT>(acc, red);  // also orders this tile's reads before the next
-    if (threadIdx.x == 0) partial[(int64_t)img * tiles + tl] = tot;
   }
 }
 
-constexpr size_t kSsimTmaSmem = 128 + 2 * (size_t)kSsimStage + (size_t)kSsimIn * 40 * 4 * 2 +
-                                (size_t)5 * kSsimIn * kSsimT * 8 + 16;
-
-constexpr size_t kSsimSmem = (size_t)(kSsimIn * 40 * 2 + 1) / 2 * 8 + (size_t)5 * kSsimIn * kSsimT * 8;
+template <typename OrigT, typename RecT>
+__global__ void __launch_bounds__(kSsNT) ssim_strip_kernel(const OrigT* __restrict__ orig,
+                                                           const RecT* __restrict__ rec, KGeom g, int32_t height,
+                                                           int32_t width, int32_t nstrips, int32_t units,
+                                                           int64_t total_units, int clip, float lo, float hi,
+                                                           double c1s, double c2s, double* __restrict__ partial) {
+  using Acc = SsAcc<OrigT>;
+  const int lane = threadIdx.x;
+  const int64_t u = blockIdx.x;
+  const int32_t img = (int32_t)(u / units), q = (int32_t)(u % units);
+  const int32_t band = q / nstrips, strip = q - band * nstrips;
+  const int32_t x = strip * kSsOut + lane, y0 = band * kSsTY;
+  const int32_t nout = min(kSsTY, height - 7 - y0);  // window rows of this band
+  const int32_t nin = nout + 7;                      // input rows it reads
+  const bool col_ok = x < width;
+  const bool win_ok = lane < kSsOut && x <= width - 8;
+  const int64_t rs = g.row_stride;
+  const int64_t base = (int64_t)img * g.image_stride + (int64_t)y0 * rs + (col_ok ? x : 0);
+  const OrigT* po = orig + base;
+  const RecT* pr = rec + base;
+  // three 8-row buffers in rotation (current, previous, prefetched next): no register copies
+  SsGroup<OrigT, RecT> g0, g1, g2;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    g2.a[k] = 0;
+    g2.b[k] = 0;
+  }
+  ss_load(g0, po, pr, rs, 0, nin, col_ok);
+  SsState<Acc> s{0, 0, 0.0, 0.0, 0.0, 0.0};
+  const int ngroups = (nin + 7) / 8;
+  for (int gi = 0; gi < ngroups; gi += 3) {
+    ss_load(g1, po + 8 * (gi + 1) * rs, pr + 8 * (gi + 1) * rs, rs, 8 * (gi + 1), nin, col_ok);
+    ss_group(s, g0, g2, gi, nout, win_ok, clip, lo, hi, c1s, c2s);
+    if (gi + 1 >= ngroups) break;
+    ss_load(g2, po + 8 * (gi + 2) * rs, pr + 8 * (gi + 2) * rs, rs, 8 * (gi + 2), nin, col_ok);
+    ss_group(s, g1, g0, gi + 1, nout, win_ok, clip, lo, hi, c1s, c2s);
+    if (gi + 2 >= ngroups) break;
+    ss_load(g0, po + 8 * (gi + 3) * rs, pr + 8 * (gi + 3) * rs, rs, 8 * (gi + 3), nin, col_ok);
+    ss_group(s, g2, g1, gi + 2, nout, win_ok, clip, lo, hi, c1s, c2s);
+  }
+  double acc = s.acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) partial[(int64_t)img * units + q] = acc;
+}
 
 }  // namespace
 
-int64_t ssim_tiles(const adct_geom& g) {
+int64_t ssim_tiles(const adct_geom& g) {  // warps (strip x band units) per image
   if (g.height < 8 || g.width < 8) return 0;
-  return (int64_t)((g.width - 7 + kSsimT - 1) / kSsimT) * ((g.height - 7 + kSsimT - 1) / kSsimT);
+  return (int64_t)((g.width - 7 + kSsOut - 1) / kSsOut) * ((g.height - 7 + kSsTY - 1) / kSsTY);
 }
 
 void launch_finalize_scaled(const double* partial, int32_t chunks, int64_t n_images, double scale, double* out,
@@ -662,59 +634,17 @@ adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
   if (g.n_images > 65535) return ADCT_E_INVALID_ARGUMENT;
   cudaStream_t st = (cudaStream_t)stream;
   const KGeom kg = make_kgeom(g);
-  const int32_t ntx = (g.width - 7 + kSsimT - 1) / kSsimT;
-  const int32_t tiles = (int32_t)ssim_tiles(g);
+  const int32_t nstrips = (g.width - 7 + kSsOut - 1) / kSsOut;
+  const int32_t units = (int32_t)ssim_tiles(g);
+  const int64_t total = (int64_t)units * g.n_images;
   const float lo = 0.0f, hi = (float)peak;  // clip range of the reconstruction: [0, peak]
   const double c1 = (0.01 * peak) * (0.01 * peak), c2 = (0.03 * peak) * (0.03 * peak);
   double* partial = (double*)workspace;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(ssim_kernel<uint8_t, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
-    cudaFuncSetAttribute(ssim_kernel<uint8_t, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
-    cudaFuncSetAttribute(ssim_kernel<uint8_t, int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
-    cudaFuncSetAttribute(ssim_kernel<int16_t, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
-    cudaFuncSetAttribute(ssim_kernel<int16_t, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
-    cudaFuncSetAttribute(ssim_kernel<int16_t, int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimSmem);
-  });
-  if (orig_t == ADCT_U8 && recon_t == ADCT_F32 && g.row_stride % 16 == 0 &&
-      (g.n_images == 1 || g.image_stride % 16 == 0) && aligned(orig, 16) && aligned(recon, 16)) {
-    auto enc = tmap_encoder();
-    CUtensorMap to, tr;
-    const cuuint64_t dims[3] = {(cuuint64_t)g.width, (cuuint64_t)g.height, (cuuint64_t)g.n_images};
-    const int64_t istr = g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride;
-    const cuuint64_t so[2] = {(cuuint64_t)g.row_stride, (cuuint64_t)istr};
-    const cuuint64_t sr[2] = {(cuuint64_t)g.row_stride * 4, (cuuint64_t)istr * 4};
-    const cuuint32_t bo[3] = {(cuuint32_t)kSsimBoxO, (cuuint32_t)kSsimIn, 1}, br[3] = {(cuuint32_t)kSsimBoxR, (cuuint32_t)kSsimIn, 1};
-    const cuuint32_t es[3] = {1, 1, 1};
-    if (enc &&
-        enc(&to, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(orig), dims, so, bo, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-            CUDA_SUCCESS &&
-        enc(&tr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(recon), dims, sr, br, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
-      static std::once_flag once_tma;
-      std::call_once(once_tma, [] {
-        cudaFuncSetAttribute(ssim_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSsimTmaSmem);
-      });
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const int64_t n_tiles = (int64_t)tiles * g.n_images;
-      const int64_t cap = (int64_t)sms * 2;
-      ssim_tma_kernel<<<(unsigned)(n_tiles < cap ? n_tiles : cap), kSsimNT, kSsimTmaSmem, st>>>(
-          to, tr, g.height, g.width, ntx, tiles, n_tiles, (int)clip, lo, hi, c1, c2, partial);
-      count_launch();
-      if (adct_status e = launch_status()) return e;
-      const double nwin = (double)(g.height - 7) * (double)(g.width - 7);
-      launch_finalize_scaled(partial, tiles, g.n_images, 1.0 / nwin, ssim, st);
-      return launch_status();
-    }
-  }
-  const dim3 grid((unsigned)tiles, (unsigned)g.n_images);
-#define ADCT_SSIM(OT, RT)                                                                                      \
-  ssim_kernel<OT, RT><<<grid, kSsimNT, kSsimSmem, st>>>((const OT*)orig, (const RT*)recon, kg, g.height, g.width, \
-                                                        ntx, tiles, (int)clip, lo, hi, c1, c2, partial)
+  const unsigned grid = (unsigned)total;
+#define ADCT_SSIM(OT, RT)                                                                                    \
+  ssim_strip_kernel<OT, RT><<<grid, kSsNT, 0, st>>>((const OT*)orig, (const RT*)recon, kg, g.height, g.width, \
+                                                    nstrips, units, total, (int)clip, lo, hi, 4096.0 * c1,    \
+                                                    4096.0 * c2, partial)
   if (orig_t == ADCT_U8) {
     if (recon_t == ADCT_F32) ADCT_SSIM(uint8_t, float); else if (recon_t == ADCT_U8) ADCT_SSIM(uint8_t, uint8_t);
     else ADCT_SSIM(uint8_t, int16_t);
@@ -726,7 +656,7 @@ adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
   count_launch();
   if (adct_status e = launch_status()) return e;
   const double nwin = (double)(g.height - 7) * (double)(g.width - 7);
-  launch_finalize_scaled(partial, tiles, g.n_images, 1.0 / nwin, ssim, st);
+  launch_finalize_scaled(partial, units, g.n_images, 1.0 / nwin, ssim, st);
   return launch_status();
 }
 

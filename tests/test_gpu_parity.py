@@ -389,15 +389,35 @@ def test_ssim_reduce_matches_oracle(shape, rtype):
         assert np.allclose(got, ref, rtol=1e-9, atol=1e-12), (got, ref)
 
 
-def test_ssim_tma_path_many_tiles_per_cta():
-    """u8 originals with fp32 reconstructions and 16-byte strides take the persistent TMA kernel;
-    enough images that every CTA walks several tiles through both ring slots."""
+def test_ssim_many_bands_and_strips():
+    """u8 originals with fp32 reconstructions over many images: every warp unit (a band of 64
+    window rows x a strip of 25 window columns) is used, including the ragged last band and
+    strip of each image, and the partials of all images are finalized independently."""
     x = images("ar1", 40, 256, 272, seed=9)
     r = (x.float() + torch.from_numpy(np.random.default_rng(1).normal(0, 9, size=x.shape).astype(np.float32)))
     for clip in (adct.CLIP_NONE, adct.CLIP):
         got = adct.ssim_reduce(x.to(DEV), r.to(DEV), clip=clip).cpu().numpy()
         ref = OS.ssim(x.numpy(), r.numpy(), clip=clip)
         assert np.allclose(got, ref, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("rtype", [torch.int16, torch.float32, torch.uint8])
+def test_ssim_int16_original(rtype):
+    """int16 originals (the fp64 sums path: x^2 window sums exceed 2^24) against the oracle,
+    with int16 / fp32 / u8 reconstructions, at shapes with one band and several, including
+    a single-window image."""
+    for n, h, w in ((1, 8, 8), (2, 72, 112), (1, 144, 40)):
+        g = np.random.default_rng(h * w)
+        x = torch.from_numpy(g.integers(-300, 300, size=(n, h, w)).astype(np.int16))
+        r = x.float() + torch.from_numpy(g.normal(0, 15, size=(n, h, w)).astype(np.float32))
+        if rtype == torch.int16:
+            r = r.round().to(torch.int16)
+        elif rtype == torch.uint8:
+            r = r.clamp(0, 255).round().to(torch.uint8)
+        for clip in (adct.CLIP_NONE, adct.CLIP, adct.CLIP_ROUND):
+            got = adct.ssim_reduce(x.to(DEV), r.to(DEV), clip=clip).cpu().numpy()
+            ref = OS.ssim(x.numpy(), r.numpy(), clip=clip)
+            assert np.allclose(got, ref, rtol=1e-9, atol=1e-12), (n, h, w, clip, got, ref)
 
 
 def test_ssim_identical_is_one_and_pipeline(mats):
