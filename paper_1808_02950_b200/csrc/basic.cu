@@ -349,14 +349,14 @@ __device__ __forceinline__ void ss_load(SsGroup<OrigT, RecT>& gr, const OrigT* p
 // rows 8 gi .. 8 gi + 7: add row r, drop row r - 8 (the previous group's slot), and for r >= 7
 // evaluate the windows whose top row is r - 7.  Padding rows / columns are 0 before and after
 // the clip (they only reach windows that are not counted).
-template <typename Acc, typename OrigT, typename RecT>
+template <int CLIP, typename Acc, typename OrigT, typename RecT>
 __device__ __forceinline__ void ss_group(SsState<Acc>& s, const SsGroup<OrigT, RecT>& cur,
-                                         const SsGroup<OrigT, RecT>& prev, int gi, int nout, bool win_ok, int clip,
-                                         float lo, float hi, double c1s, double c2s) {
+                                         const SsGroup<OrigT, RecT>& prev, int gi, int nout, bool win_ok, float lo,
+                                         float hi, double c1s, double c2s) {
   auto y_of = [&](RecT v) {
     float b = (float)v;
-    if (clip != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
-    if (clip == ADCT_CLIP_ROUND) b = rintf(b);
+    if constexpr (CLIP != ADCT_CLIP_NONE) b = fminf(fmaxf(b, lo), hi);
+    if constexpr (CLIP == ADCT_CLIP_ROUND && std::is_same_v<RecT, float>) b = rintf(b);
     return (double)b;
   };
 #pragma unroll
@@ -383,11 +383,11 @@ __device__ __forceinline__ void ss_group(SsState<Acc>& s, const SsGroup<OrigT, R
   }
 }
 
-template <typename OrigT, typename RecT>
+template <typename OrigT, typename RecT, int CLIP>
 __global__ void __launch_bounds__(kSsNT) ssim_strip_kernel(const OrigT* __restrict__ orig,
                                                            const RecT* __restrict__ rec, KGeom g, int32_t height,
                                                            int32_t width, int32_t nstrips, int32_t units,
-                                                           int64_t total_units, int clip, float lo, float hi,
+                                                           int64_t total_units, float lo, float hi,
                                                            double c1s, double c2s, double* __restrict__ partial) {
   using Acc = SsAcc<OrigT>;
   const int lane = threadIdx.x;
@@ -415,13 +415,13 @@ __global__ void __launch_bounds__(kSsNT) ssim_strip_kernel(const OrigT* __restri
   const int ngroups = (nin + 7) / 8;
   for (int gi = 0; gi < ngroups; gi += 3) {
     ss_load(g1, po + 8 * (gi + 1) * rs, pr + 8 * (gi + 1) * rs, rs, 8 * (gi + 1), nin, col_ok);
-    ss_group(s, g0, g2, gi, nout, win_ok, clip, lo, hi, c1s, c2s);
+    ss_group<CLIP>(s, g0, g2, gi, nout, win_ok, lo, hi, c1s, c2s);
     if (gi + 1 >= ngroups) break;
     ss_load(g2, po + 8 * (gi + 2) * rs, pr + 8 * (gi + 2) * rs, rs, 8 * (gi + 2), nin, col_ok);
-    ss_group(s, g1, g0, gi + 1, nout, win_ok, clip, lo, hi, c1s, c2s);
+    ss_group<CLIP>(s, g1, g0, gi + 1, nout, win_ok, lo, hi, c1s, c2s);
     if (gi + 2 >= ngroups) break;
     ss_load(g0, po + 8 * (gi + 3) * rs, pr + 8 * (gi + 3) * rs, rs, 8 * (gi + 3), nin, col_ok);
-    ss_group(s, g2, g1, gi + 2, nout, win_ok, clip, lo, hi, c1s, c2s);
+    ss_group<CLIP>(s, g2, g1, gi + 2, nout, win_ok, lo, hi, c1s, c2s);
   }
   double acc = s.acc;
 #pragma unroll
@@ -641,10 +641,16 @@ adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
   const double c1 = (0.01 * peak) * (0.01 * peak), c2 = (0.03 * peak) * (0.03 * peak);
   double* partial = (double*)workspace;
   const unsigned grid = (unsigned)total;
-#define ADCT_SSIM(OT, RT)                                                                                    \
-  ssim_strip_kernel<OT, RT><<<grid, kSsNT, 0, st>>>((const OT*)orig, (const RT*)recon, kg, g.height, g.width, \
-                                                    nstrips, units, total, (int)clip, lo, hi, 4096.0 * c1,    \
-                                                    4096.0 * c2, partial)
+#define ADCT_SSIM_C(OT, RT, C)                                                                     \
+  ssim_strip_kernel<OT, RT, C><<<grid, kSsNT, 0, st>>>((const OT*)orig, (const RT*)recon, kg, g.height, g.width, \
+                                                       nstrips, units, total, lo, hi, 4096.0 * c1, 4096.0 * c2,  \
+                                                       partial)
+#define ADCT_SSIM(OT, RT)                                                  \
+  do {                                                                     \
+    if (clip == ADCT_CLIP_NONE) ADCT_SSIM_C(OT, RT, ADCT_CLIP_NONE);       \
+    else if (clip == ADCT_CLIP) ADCT_SSIM_C(OT, RT, ADCT_CLIP);            \
+    else ADCT_SSIM_C(OT, RT, ADCT_CLIP_ROUND);                             \
+  } while (0)
   if (orig_t == ADCT_U8) {
     if (recon_t == ADCT_F32) ADCT_SSIM(uint8_t, float); else if (recon_t == ADCT_U8) ADCT_SSIM(uint8_t, uint8_t);
     else ADCT_SSIM(uint8_t, int16_t);
@@ -653,6 +659,7 @@ adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
     else ADCT_SSIM(int16_t, int16_t);
   }
 #undef ADCT_SSIM
+#undef ADCT_SSIM_C
   count_launch();
   if (adct_status e = launch_status()) return e;
   const double nwin = (double)(g.height - 7) * (double)(g.width - 7);
