@@ -165,6 +165,24 @@ def run_reference(args):
     return 0
 
 
+def issue_roofline(case, ms, clk, dev):
+    """Roofline of an ALU-bound line: warp-instructions per step (ncu smsp__inst_executed.sum,
+    profiles/ncu_instructions.json via tools/inst_table.py) / step time against the issue peak
+    SMs x 4 SMSPs x 1 warp-instruction/clk at the SM clock sampled during the run."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_instructions.json")) as f:
+            inst = json.load(f)[case]["warp_inst_per_step"]
+    except (OSError, KeyError, ValueError):
+        return {"bound": "alu", "achieved": None, "peak": None, "unit": "warp-inst/s", "frac": None,
+                "note": "no instruction count recorded (tools/gpu/ncu_inst.sh)"}
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * 4 * (clk.get("sm_mhz") or 1965) * 1e6
+    achieved = inst / (ms * 1e-3)
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "warp-inst/s", "frac": achieved / peak,
+            "peak_kind": "issue: SMs x 4 SMSP x 1 warp-inst/clk x sampled SM clock", "traffic": None,
+            "warp_inst_per_step": inst, "inst_source": "profiles/ncu_instructions.json (ncu, same command)"}
+
+
 def _timed(fn, steps, warmup, stream, dev):
     """Mean CUDA-event time (ms) of fn() over `steps` launches after `warmup` (one stream)."""
     for _ in range(warmup):
@@ -193,14 +211,14 @@ def run_config(args):
     hbm_peak, peak_kind = peaks()
     lines = []
 
-    def emit(cfg, matrix, ms, blocks, bytes_per_block, bound, clk, cpu, extra=None):
+    def emit(cfg, matrix, ms, blocks, bytes_per_block, bound, clk, cpu, extra=None, roofline=None):
         achieved = blocks * bytes_per_block / (ms * 1e-3) / 1e9
         line = {"metric": METRIC, "value": blocks / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f32",
                 "data": "synthetic", "config": {"workload": cfg, "matrix": matrix},
-                "roofline": {"bound": bound, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                             "frac": achieved / hbm_peak, "peak_kind": peak_kind,
-                             "bytes_per_block": bytes_per_block},
+                "roofline": roofline or {"bound": bound, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                                         "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                                         "bytes_per_block": bytes_per_block},
                 "clocks": clk, "cpu_baseline": cpu}
         if extra:
             line.update(extra)
@@ -273,7 +291,8 @@ def run_config(args):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f64",
                 "data": "the nine matrices of C2", "config": {"workload": "MERIT (next row f4): Table 4 measures of 9 "
                                                               "matrices x 4096 rho (Fig. 1 curves)"},
-                "roofline": {"bound": "alu", "note": "fp64 8x8 products per thread; launch-latency sized"},
+                "roofline": dict(issue_roofline("MERIT", ms, clk, dev),
+                                 note="fp64 8x8 products per thread; one launch of 9 x 4096 threads: latency sized"),
                 "clocks": clk, "fig1_max_cg_gap_T1_minus_DCT_dB": float((out[t1, :, 2] - out[dct, :, 2]).max()),
                 "cpu_baseline": {"value": 1.0 / cdt, "unit": "(matrix, rho)/s", "cores": 1, "kind": "oracle",
                                  "sample": "256 rho values, C*_g of T1 only (numpy oracle)"}}
@@ -307,7 +326,8 @@ def run_config(args):
                     "higher_is_better": True, "dtype": "f64 score / int8 dp4a orthogonality", "data": "exact DCT C",
                     "config": {"workload": f"GREEDY (next row f3): {name}", "feasible": int((st == 0).sum()),
                                "infeasible": int((st == 1).sum()), "distinct_matrices": distinct},
-                    "roofline": {"bound": "alu", "note": "candidate scan: DP4A orthogonality + fp64 score loads"},
+                    "roofline": dict(issue_roofline("GREEDY D2" if fixed else "GREEDY D1", ms, clk, dev),
+                                     note="candidate scan: DP4A orthogonality + fp64 score loads"),
                     "clocks": clk,
                     "cpu_baseline": {"value": nsmp * (8 - len(fixed or {})) * len(ent) ** 8 / cdt,
                                      "unit": "candidates/s", "cores": 1, "kind": "oracle",
@@ -365,7 +385,8 @@ def run_config(args):
             cpu = cpu_rate(lambda: oracle.codec_sse(img.cpu().numpy(), rs, t=OM.T1), 4096)
             cpu["sample"] = "the same image, r = 1..64"
             emit("C1: one 512x512 AR(1) image, T1, fwd -> retain r -> inv -> PSNR for every r = 1..64", "T1", ms,
-                 4096, 64, "latency", clk, cpu)
+                 4096, 64, "hbm", clk, cpu, extra={"note": "one 512x512 image (256 KB): launch-latency bound, "
+                                                          "the HBM fraction is not meaningful"})
         if args.config in ("C2", "all"):
             rho, std = synth.config2_params(45, 2)
             imgs = synth.ar1_stack(45, 512, 512, rho, std=std, seed=2, device=dev, batch=15)
@@ -384,7 +405,7 @@ def run_config(args):
             cpu["sample"] = "image 0, T1, r = 1..64"
             emit("C2: 45 AR(1) 512x512 images, r = 1..64 curves for the 9 matrices (T1, C, T2, LO, SDCT, RDCT, "
                  "BAS-2008b, T4, T6) through the same kernel; value counts block x matrix", "all 9", ms,
-                 45 * 4096 * 9, 64, "alu", clk, cpu)
+                 45 * 4096 * 9, 64, "alu", clk, cpu, roofline=issue_roofline("C2", ms, clk, dev))
     return 0
 
 
