@@ -187,8 +187,10 @@ __device__ __forceinline__ int64_t jam_row_offset(uint32_t b, int i, const KGeom
 }
 
 // Persistent (grid = SMs x resident CTAs).  The next iteration's row is loaded into registers
-// right after pass 1 consumes the current one, so its HBM latency overlaps passes 2-3.  Two
-// barriers per iteration: pass 3 and the next pass 1 touch only the thread's own row.
+// right after pass 1 consumes the current one, so its HBM latency overlaps passes 2-3.  A warp
+// owns whole blocks (N = 32: one, N = 16: two), so every shared-memory exchange stays inside the
+// warp: two __syncwarp per iteration, no CTA barrier (pass 3 and the next pass 1 touch only the
+// thread's own row).
 template <int N, typename SrcT>
 __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_MINB32) jam_roundtrip_kernel(const SrcT* __restrict__ src, KGeom g, JamW<N> wt,
                                                                uint32_t nblocks, FastDiv dnbi, FastDiv dbw,
@@ -196,6 +198,8 @@ __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_M
                                                                void* __restrict__ recon) {
   constexpr int BPC = kJamNT / N;  // blocks per CTA
   constexpr bool kSat16 = sizeof(SrcT) == 2;
+  static_assert(32 % N == 0 || N % 32 == 0, "a warp must own whole blocks");
+  static_assert(N <= 32, "one block per warp at most");
   // row pitch N + 4 floats = an odd number of 16-byte units: 128-bit row accesses (8 lanes per
   // phase, rows i..i+7) and scalar column accesses (consecutive columns) are both conflict-free
   constexpr int P = N + 4;
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_M
     const int64_t offn = vn ? jam_row_offset<N>(bn, i, g, dnbi, dbw) : 0;
     if (vn) raw.load(src + offn);
     else raw.zero();
-    __syncthreads();
+    __syncwarp();
     {  // pass 2: column i (frequency l = i) of block bl: forward, weights, inverse
       float c[N], y[N];
 #pragma unroll
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_M
 #pragma unroll
       for (int k = 0; k < N; ++k) sm[(bl * N + k) * P + i] = c[k];
     }
-    __syncthreads();
+    __syncwarp();
     {  // pass 3: row i, inverse, store
       float z[N], x[N];
 #pragma unroll
