@@ -440,11 +440,11 @@ def main():
     geoms = [adct.geom_of(p) for p in planes]
     ws = torch.empty(max(adct.workspace_bytes(g, 1) for g in geoms), dtype=torch.uint8, device=dev)
     # global per-frame, per-plane table (fp64): `local` holds this rank's rows (the others stay
-    # zero); every step it is copied into `table` and all-reduced, so each entry has exactly one
-    # non-zero contributor and the result is bit-identical to a single GPU
+    # zero; the kernels write their per-frame SSE straight into it); every step it is copied into
+    # `table` and all-reduced, so each entry has exactly one non-zero contributor and the result
+    # is bit-identical to a single GPU
     etab = parallel.ErrorTable(world * FRAMES, 3, rank * FRAMES, (rank + 1) * FRAMES, device=dev)
     table = etab.table
-    sse_planes = [torch.empty((FRAMES, 1), dtype=torch.float64, device=dev) for _ in range(3)]
     lo = rank * FRAMES
 
     # per-step events around the luma launch (the dominant kernel), on the launching stream
@@ -455,10 +455,9 @@ def main():
         for i, p in enumerate(planes):
             if k is not None and i == 0:
                 ev_luma[k][0].record(stream)
-            adct.approx_dct8x8_fused_sse(m, p, [R], workspace=ws, sse=sse_planes[i], stream=stream)
+            adct.approx_dct8x8_fused_sse(m, p, [R], workspace=ws, sse=etab.out(i), stream=stream)
             if k is not None and i == 0:
                 ev_luma[k][1].record(stream)
-            etab.set_local(i, sse_planes[i])
         etab.combine()
 
     for _ in range(args.warmup):

@@ -123,6 +123,21 @@ def _stream_ptr(stream) -> int | None:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _out(t: torch.Tensor, numel: int, like: torch.Tensor, name: str, dtype=None, host: bool = False) -> torch.Tensor:
+    """A caller-provided output tensor: the library writes `numel` contiguous elements through its
+    data pointer, so the dtype, contiguity, size and device are checked before any launch."""
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.numel() < numel:
+        raise ValueError(f"{name} holds {t.numel()} elements, {numel} needed")
+    want = torch.device("cpu") if host else like.device
+    if t.device != want:
+        raise ValueError(f"{name} must be on {want}, got {t.device}")
+    return t
+
+
 def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -214,6 +229,7 @@ def approx_dct8x8_fwd(m: Matrix, src: torch.Tensor, coef_dtype=torch.int32, coef
     g = geom_of(src)
     if coef is None:
         coef = torch.empty((g.n_images, g.height // 8, g.width // 8, 8, 8), dtype=coef_dtype, device=src.device)
+    _out(coef, g.n_images * g.height * g.width, src, "coef")
     _check(lib.approx_dct8x8_fwd(m.handle, src.data_ptr(), dtype_code(src), g, coef.data_ptr(), dtype_code(coef),
                                  _stream_ptr(stream)), "approx_dct8x8_fwd")
     return coef
@@ -234,6 +250,8 @@ def approx_dct8x8_inv(m: Matrix, coef: torch.Tensor, height: int, width: int, re
     if recon is None:
         recon = torch.empty((n, height, width), dtype=recon_dtype, device=coef.device)
     g = geom_of(recon)
+    if not coef.is_contiguous() or coef.numel() < g.n_images * g.height * g.width or coef.device != recon.device:
+        raise ValueError("coef must be contiguous block-major [n, H/8, W/8, 8, 8] on recon's device")
     _check(lib.approx_dct8x8_inv(m.handle, coef.data_ptr(), dtype_code(coef), g, recon.data_ptr(),
                                  dtype_code(recon), int(clip), _stream_ptr(stream)), "approx_dct8x8_inv")
     return recon
@@ -265,8 +283,10 @@ def approx_dct_jam_roundtrip(n: int, src: torch.Tensor, r: int, recon_dtype=torc
     g = geom_of(src)
     if recon is None:
         recon = torch.empty_strided(tuple(src.shape), src.stride(), dtype=recon_dtype, device=src.device)
-    if tuple(recon.stride()) != tuple(src.stride()):
-        raise ValueError("recon must have the strides of src")
+    if tuple(recon.stride()) != tuple(src.stride()) or tuple(recon.shape) != tuple(src.shape):
+        raise ValueError("recon must have the shape and strides of src")
+    if recon.device != src.device:
+        raise ValueError("recon must be on src's device")
     _check(lib.approx_dct_jam_roundtrip(int(n), src.data_ptr(), dtype_code(src), g, int(r), recon.data_ptr(),
                                         dtype_code(recon), int(clip), _stream_ptr(stream)), "approx_dct_jam_roundtrip")
     return recon
@@ -343,8 +363,10 @@ def approx_dct8x8_roundtrip(m: Matrix, src: torch.Tensor, r: int = 64, recon_dty
     if recon is None:
         recon = torch.empty_strided(tuple(src.shape[-3:]) if src.dim() == 3 else tuple(src.shape),
                                     src.stride(), dtype=recon_dtype, device=src.device)
-    if tuple(recon.stride()) != tuple(src.stride()):
-        raise ValueError("recon must have the strides of src")
+    if tuple(recon.stride()) != tuple(src.stride()) or tuple(recon.shape) != tuple(src.shape):
+        raise ValueError("recon must have the shape and strides of src")
+    if recon.device != src.device:
+        raise ValueError("recon must be on src's device")
     _check(lib.approx_dct8x8_roundtrip(m.handle, src.data_ptr(), dtype_code(src), g, int(r), recon.data_ptr(),
                                        dtype_code(recon), int(clip), _stream_ptr(stream)),
            "approx_dct8x8_roundtrip")
@@ -360,6 +382,7 @@ def approx_dct8x8_fused_sse(m: Matrix, src: torch.Tensor, r_list, clip: int = CL
     arr = (ctypes.c_int32 * len(rl))(*rl)
     if sse is None:
         sse = torch.empty((g.n_images, len(rl)), dtype=torch.float64, device=src.device)
+    _out(sse, g.n_images * len(rl), src, "sse", dtype=torch.float64)
     nbytes = workspace_bytes(g, len(rl))
     if workspace is None or workspace.numel() < nbytes:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=src.device)
@@ -383,6 +406,7 @@ def approx_dct8x8_fused_sse_host(m: Matrix, src_host: torch.Tensor, r_list, work
     arr = (ctypes.c_int32 * len(rl))(*rl)
     if sse_host is None:
         sse_host = torch.empty((g.n_images, len(rl)), dtype=torch.float64)
+    _out(sse_host, g.n_images * len(rl), src_host, "sse_host", dtype=torch.float64, host=True)
     _check(lib.approx_dct8x8_fused_sse_host(m.handle, src_host.data_ptr(), dtype_code(src_host), g,
                                             ctypes.cast(arr, ctypes.c_void_p), len(rl), int(clip),
                                             sse_host.data_ptr(), int(chunk_images), workspace.data_ptr(),
@@ -395,6 +419,7 @@ def approx_dct8x8_fwd_quant(m: Matrix, src: torch.Tensor, step: int = 16, q: tor
     g = geom_of(src)
     if q is None:
         q = torch.empty((g.n_images, g.height // 8, g.width // 8, 8, 8), dtype=torch.int16, device=src.device)
+    _out(q, g.n_images * g.height * g.width, src, "q", dtype=torch.int16)
     _check(lib.approx_dct8x8_fwd_quant(m.handle, src.data_ptr(), g, int(step), q.data_ptr(), _stream_ptr(stream)),
            "approx_dct8x8_fwd_quant")
     return q

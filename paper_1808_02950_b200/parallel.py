@@ -57,19 +57,27 @@ class ErrorTable:
     `local` holds this rank's rows [lo, hi) and zeros elsewhere; `combine()` copies it into the
     output and all-reduces (SUM), so every entry has exactly one non-zero contributor and the
     result is bit-identical to a single-process run however often it is combined.  (All-reducing
-    the output in place step after step would add the other ranks' stale copies.)"""
+    the output in place step after step would add the other ranks' stale copies.)  Storage is
+    column-major, so `out(col)` -- this rank's rows of one column -- is contiguous and a kernel
+    writes its per-image results there directly; `local` and `table` are [n_total, cols] views."""
 
     def __init__(self, n_total: int, cols: int, lo: int, hi: int, device=None):
         self.lo, self.hi = lo, hi
-        self.local = torch.zeros((n_total, cols), dtype=torch.float64, device=device)
-        self.table = torch.zeros_like(self.local)
+        self._local = torch.zeros((cols, n_total), dtype=torch.float64, device=device)
+        self._table = torch.zeros_like(self._local)
+        self.local = self._local.t()
+        self.table = self._table.t()
+
+    def out(self, col: int) -> torch.Tensor:
+        return self._local[col, self.lo:self.hi]
 
     def set_local(self, col: int, values: torch.Tensor) -> None:
-        self.local[self.lo:self.hi, col:col + 1].copy_(values.reshape(self.hi - self.lo, 1))
+        self.out(col).copy_(values.reshape(self.hi - self.lo))
 
     def combine(self) -> torch.Tensor:
-        self.table.copy_(self.local)
-        return combine_error_table(self.table)
+        self._table.copy_(self._local)
+        combine_error_table(self._table)
+        return self.table
 
 
 def combine_error_table(local: torch.Tensor) -> torch.Tensor:

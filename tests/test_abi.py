@@ -7,6 +7,7 @@ import re
 
 import numpy as np
 import pytest
+import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -173,3 +174,25 @@ def test_argument_validation_next_rows():
     assert L.ssim_reduce(fake, adct.U8, fake, adct.F32, _fake(), 255.0, 0, fake, fake, 8, None) == 7
     # merit: negative counts
     assert L.adct_merit_batch(cp, fake, fake, -1, fake, 4, fake, None) == 1
+
+
+def test_binding_validates_caller_outputs():
+    """Output tensors a caller passes are written through their data pointer, so the binding
+    checks dtype, contiguity, size and shape before any call reaches the library (CPU tensors:
+    the checks run before any launch)."""
+    m = adct.Matrix.from_int(catalog.T1)
+    src = torch.zeros((2, 16, 16), dtype=torch.uint8)
+    with pytest.raises(ValueError):
+        adct.approx_dct8x8_fused_sse(m, src, [10], sse=torch.empty((2, 1), dtype=torch.float32))
+    with pytest.raises(ValueError):
+        adct.approx_dct8x8_fused_sse(m, src, [3, 10], sse=torch.empty((2, 1), dtype=torch.float64))
+    with pytest.raises(ValueError):
+        adct.approx_dct8x8_fused_sse(m, src, [10], sse=torch.empty((2, 2), dtype=torch.float64)[:, :1])
+    with pytest.raises(ValueError):
+        adct.approx_dct8x8_fwd_quant(m, src, q=torch.empty((2, 2, 2, 8, 8), dtype=torch.int32))
+    with pytest.raises(ValueError):
+        adct.approx_dct8x8_fwd(m, src, coef=torch.empty((1, 2, 2, 8, 8), dtype=torch.int32))
+    with pytest.raises(ValueError):
+        adct.approx_dct8x8_roundtrip(m, src, 10, recon=torch.empty((1, 16, 16), dtype=torch.int16))
+    with pytest.raises(ValueError):
+        adct.approx_dct_jam_roundtrip(16, src, 10, recon=torch.empty((2, 16, 8), dtype=torch.float32))

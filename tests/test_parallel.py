@@ -85,3 +85,18 @@ def test_error_table_allreduce_is_bit_identical(world):
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in res)
     assert all(t == world - 0.5 for _, _, t in res)  # max over ranks
+
+
+def test_error_table_out_views_are_contiguous_rank_rows():
+    """ErrorTable.out(col) is where a kernel writes one column of this rank's rows: contiguous,
+    aliasing `local`, and combine() returns the [n_total, cols] table."""
+    et = parallel.ErrorTable(10, 3, 4, 7)
+    for c in range(3):
+        o = et.out(c)
+        assert o.is_contiguous() and o.shape == (3,)
+        o.copy_(torch.arange(3, dtype=torch.float64) + 10 * c)
+    tab = et.combine()
+    assert tab.shape == (10, 3)
+    assert torch.equal(tab[4:7], et.local[4:7])
+    assert torch.equal(tab[4:7, 2], torch.tensor([20.0, 21.0, 22.0], dtype=torch.float64))
+    assert float(tab[:4].abs().sum()) == 0.0 and float(tab[7:].abs().sum()) == 0.0
