@@ -23,6 +23,12 @@ __global__ void __launch_bounds__(1024) pipe_kernel(const uint32_t* in, uint32_t
 #pragma unroll
   for (int i = 0; i < 8; ++i) f2[i] = make_float2(__uint_as_float(r[i]) , __uint_as_float(r[(i + 3) & 7]));
   float2 fa = make_float2(__uint_as_float(a0), __uint_as_float(a1));
+  float d[8][4], g[8][4];
+  uint32_t di[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { d[i][u] = 0.f; g[i][u] = __uint_as_float(r[(i + u) & 7]); di[i][u] = r[u]; }
   __syncthreads();
   long long t0 = clock64();
 #pragma unroll 16
@@ -70,12 +76,29 @@ __global__ void __launch_bounds__(1024) pipe_kernel(const uint32_t* in, uint32_t
         asm volatile("{.reg .b32 t; shr.b32 t, %0, 8; cvt.rn.f32.u8 %0, t;}" : "+r"(r[i]));
       }
       if (OP == 24) asm volatile("cvt.rn.f32.u8 %0, %0;" : "+r"(r[i]));  // I2F.U8 .B0
+      if (OP == 25 || OP == 26)  // HMMA m16n8k16 f16 -> f32 (legacy mma.sync)
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                     : "+f"(d[i][0]), "+f"(d[i][1]), "+f"(d[i][2]), "+f"(d[i][3])
+                     : "r"(r[i]), "r"(r[(i + 1) & 7]), "r"(a0), "r"(a1), "r"(r[(i + 2) & 7]), "r"(a0));
+      if (OP == 27 || OP == 28)  // IMMA m16n8k32 u8 x s8 -> s32
+        asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                     : "+r"(di[i][0]), "+r"(di[i][1]), "+r"(di[i][2]), "+r"(di[i][3])
+                     : "r"(r[i]), "r"(r[(i + 1) & 7]), "r"(a0), "r"(a1), "r"(r[(i + 2) & 7]), "r"(a0));
+      if (OP == 26 || OP == 28) {  // + 4 independent FFMA per MMA
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(g[i][u]) : "r"(a0), "r"(a1));
+      }
     }
   }
   long long t1 = clock64();
   uint32_t acc = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc ^= r[i] ^ __float_as_uint(f2[i].x) ^ __float_as_uint(f2[i].y);
+  for (int i = 0; i < 8; ++i) {
+    acc ^= r[i] ^ __float_as_uint(f2[i].x) ^ __float_as_uint(f2[i].y);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc ^= __float_as_uint(d[i][u]) ^ __float_as_uint(g[i][u]) ^ di[i][u];
+  }
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
@@ -115,7 +138,8 @@ __global__ void read_blocks_u8(const uint8_t* __restrict__ img, int W, int H, in
 static const char* names[] = {"FFMA(3reg)", "FFMA(imm)", "FADD", "FFMA2", "FADD2", "IADD3", "LOP3", "PRMT", "LEA",
                               "IMAD", "I2FP.U32", "HFMA2", "FFMA2+IADD3", "FFMA+IADD3", "I2F.S32", "FMUL", "FMUL2",
                               "FFMA(acc a*a+d)", "FADD(sub)", "I2F.U8.B1", "I2F.U8.B1+FFMA", "I2F.S16.H1",
-                              "PRMT+FFMA", "FFMA+FADD+I2F.U8", "I2F.U8.B0"};
+                              "PRMT+FFMA", "FFMA+FADD+I2F.U8", "I2F.U8.B0", "HMMA.16816.F32",
+                              "HMMA+4FFMA", "IMMA.16832.S32", "IMMA+4FFMA"};
 
 template <int OP>
 int run_one(const uint32_t* din, uint32_t* dout, long long* dcyc, int nsm) {
@@ -129,7 +153,7 @@ int run_one(const uint32_t* din, uint32_t* dout, long long* dcyc, int nsm) {
   double mean = 0;
   for (int i = 0; i < nsm; ++i) mean += (double)h[i];
   mean /= nsm;
-  int per = (OP == 12 || OP == 13 || OP == 20 || OP == 22) ? 16 : (OP == 23 ? 24 : 8);
+  int per = (OP == 12 || OP == 13 || OP == 20 || OP == 22) ? 16 : (OP == 23 ? 24 : (OP == 26 || OP == 28) ? 40 : 8);
   double warp_inst = 32.0 * ITERS * per;  // warp-instructions per SM (32 warps)
   printf("%-18s %7.3f warp-inst/clk/SM  (%5.3f per SMSP)\n", names[OP], warp_inst / mean, warp_inst / mean / 4);
   return 0;
@@ -159,6 +183,8 @@ int main() {
   run_one<18>(din, dout, dcyc, nsm); run_one<19>(din, dout, dcyc, nsm); run_one<20>(din, dout, dcyc, nsm);
   run_one<21>(din, dout, dcyc, nsm); run_one<22>(din, dout, dcyc, nsm); run_one<23>(din, dout, dcyc, nsm);
   run_one<24>(din, dout, dcyc, nsm);
+  run_one<25>(din, dout, dcyc, nsm); run_one<26>(din, dout, dcyc, nsm); run_one<27>(din, dout, dcyc, nsm);
+  run_one<28>(din, dout, dcyc, nsm);
   if (getenv("PIPES_ONLY")) return 0;
 
   // streaming read bandwidth
