@@ -80,14 +80,21 @@ inline int64_t sse_chunks(const adct_geom& g) { return (g.height + kSseRows - 1)
 // completes on the warp's own mbarrier.  No producer warp and no cross-warp barrier: each warp
 // refills the slot it just consumed.  A chunk is kWtChunkTiles consecutive tiles of one image;
 // per-(chunk, warp) fp64 partials keep the per-image sums independent of the grid.
-constexpr int kWtWarps = 16;
+#ifndef ADCT_WT_WARPS
+#define ADCT_WT_WARPS 16
+#endif
+constexpr int kWtWarps = ADCT_WT_WARPS;
 constexpr int kWtThreads = 32 * kWtWarps;
 #ifndef ADCT_WT_BPL
 #define ADCT_WT_BPL 2
 #endif
 constexpr int kWtBPL = ADCT_WT_BPL;                 // blocks per lane per tile
 constexpr int kWtTileBytes = 2048 * kWtBPL;         // 32 * kWtBPL blocks of 64 bytes
-constexpr int kWtSlots = kWtBPL == 2 ? 3 : 2;       // ring depth (192 KB of shared memory)
+#ifndef ADCT_WT_SLOTS
+#define ADCT_WT_SLOTS 3
+#endif
+constexpr int kWtSlots = ADCT_WT_SLOTS;             // ring depth (16 x 3 x 4 KB = 192 KB of shared memory)
+static_assert((size_t)kWtWarps * kWtSlots * kWtTileBytes <= 200 * 1024, "warp-tile rings exceed shared memory");
 #ifndef ADCT_WT_CHUNK
 #define ADCT_WT_CHUNK 16
 #endif

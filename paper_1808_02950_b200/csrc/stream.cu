@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   for (int s = 0; s < kWtSlots; ++s)
     if (pf.cg < a.n_chunks) issue(s);
 
-  // lane -> block column (lane % BPR) and its two bands 2*(lane / BPR), 2*(lane / BPR) + 1
-  const uint32_t lane_u32 = ring0 + (uint32_t)(lane % BPR) * 8u + (uint32_t)(lane / BPR) * 16u * TW;
+  // lane -> block column (lane % BPR) and its kWtBPL consecutive bands from kWtBPL*(lane / BPR)
+  const uint32_t lane_u32 = ring0 + (uint32_t)(lane % BPR) * 8u + (uint32_t)(lane / BPR) * (8u * kWtBPL) * TW;
   int slot = 0;
   uint32_t phase = 0;
   WtIt it;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
     mbar_wait(&wfull[slot], phase);
     const uint32_t p = lane_u32 + (uint32_t)slot * kWtTileBytes;
 #pragma unroll kWtUnroll
-    for (int b = 0; b < 2; ++b) {  // the lane's two blocks (consecutive bands of the tile)
+    for (int b = 0; b < kWtBPL; ++b) {  // the lane's blocks (consecutive bands of the tile)
       uint2 rows[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) rows[i] = lds64(p + (uint32_t)(b * 8 + i) * TW);
