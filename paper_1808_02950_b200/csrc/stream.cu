@@ -217,6 +217,33 @@ __device__ __forceinline__ bool wt_next(const WtArgs& a, int w, WtIt& it) {
   return true;
 }
 
+// The consumer's view of the same walk: only the chunk and the tiles left in it (the tile
+// coordinates are needed by the prefetch walk alone).
+struct WcIt {
+  uint32_t cg;
+  int32_t left;  // tiles of chunk cg this warp has still to consume
+};
+
+__device__ __forceinline__ void wc_enter(const WtArgs& a, int w, WcIt& it) {
+  while (it.cg < a.n_chunks) {
+    const uint32_t img = fdiv(it.cg, a.dcpi);
+    const int32_t c = (int32_t)(it.cg - img * (uint32_t)a.cpi);
+    const int32_t n = min(kWtChunkTiles, a.tpi - c * kWtChunkTiles);
+    if (w < n) {
+      it.left = (n - 1 - w) / kWtWarps + 1;  // tiles w, w + kWtWarps, ... < n
+      return;
+    }
+    it.cg += gridDim.x;
+  }
+}
+
+__device__ __forceinline__ bool wc_next(const WtArgs& a, int w, WcIt& it) {
+  if (--it.left > 0) return false;
+  it.cg += gridDim.x;
+  wc_enter(a, w, it);
+  return true;
+}
+
 #ifndef ADCT_WT_UNROLL
 #define ADCT_WT_UNROLL 2
 #endif
@@ -264,9 +291,9 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   const uint32_t lane_u32 = ring0 + (uint32_t)(lane % BPR) * 8u + (uint32_t)(lane / BPR) * (8u * kWtBPL) * TW;
   int slot = 0;
   uint32_t phase = 0;
-  WtIt it;
+  WcIt it;
   it.cg = blockIdx.x;
-  wt_enter(a, w, it);
+  wc_enter(a, w, it);
   float acc = 0.0f;
   // chunks in which this warp has no tile keep a zero partial
   if (lane == 0)
@@ -287,7 +314,7 @@ __global__ void __launch_bounds__(kWtThreads, 1)
     if (pf.cg < a.n_chunks) issue(slot);
     if (++slot == kWtSlots) { slot = 0; phase ^= 1u; }
     const uint32_t cg = it.cg;
-    if (wt_next(a, w, it)) {  // chunk done: per-(chunk, warp) partial in a fixed shuffle order
+    if (wc_next(a, w, it)) {  // chunk done: per-(chunk, warp) partial in a fixed shuffle order
       double v = (double)acc;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
