@@ -172,6 +172,7 @@ __device__ __forceinline__ float block_sse_u8s(const MP& m, const uint2 (&rows)[
 // ---- warp-tile kernel ----------------------------------------------------------------------------
 struct WtArgs {
   int32_t tpb, tpi, cpi;  // tiles per band pair / per image, chunks per image
+  int32_t adv_pair, adv_slice;  // kWtWarps tiles = adv_pair tile rows + adv_slice tiles (adv_slice < tpb)
   uint32_t n_chunks;
   FastDiv dcpi, dtpb;
 };
@@ -205,8 +206,9 @@ __device__ __forceinline__ void wt_enter(const WtArgs& a, int w, WtIt& it) {
 __device__ __forceinline__ bool wt_next(const WtArgs& a, int w, WtIt& it) {
   ++it.j;
   if (w + kWtWarps * it.j < it.n) {
-    it.slice += kWtWarps;
-    while (it.slice >= a.tpb) {
+    it.slice += a.adv_slice;  // both < tpb: at most one carry
+    it.pair += a.adv_pair;
+    if (it.slice >= a.tpb) {
       it.slice -= a.tpb;
       ++it.pair;
     }
@@ -424,6 +426,8 @@ bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& 
     a.n_chunks = (uint32_t)p.n_chunks;
     a.dcpi = make_fastdiv((uint32_t)p.cpi);
     a.dtpb = make_fastdiv((uint32_t)p.tpb);
+    a.adv_pair = kWtWarps / p.tpb;
+    a.adv_slice = kWtWarps % p.tpb;
     const bool ok = m->specialized ? launch_wtile<T1Mat>(r, p.tw, map, a, m->dev, partial, st)
                                    : launch_wtile<RtMat>(r, p.tw, map, a, m->dev, partial, st);
     if (!ok) return false;
