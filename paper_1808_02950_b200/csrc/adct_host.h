@@ -111,13 +111,13 @@ struct WtPlan {
   int64_t n_chunks;
   bool ok;
 };
-inline WtPlan wt_plan(const adct_geom& g) {
+inline WtPlan tile_plan(const adct_geom& g, int tile_bytes, int chunk_tiles) {
   WtPlan p{};
   const int64_t W = g.width, H = g.height;
   if (W <= 0 || H <= 0) return p;
   int64_t best = -1;
   for (int tw : {256, 128}) {
-    const int64_t rows = kWtTileBytes / tw;
+    const int64_t rows = tile_bytes / tw;
     const int64_t tiles = ((W + tw - 1) / tw) * ((H + rows - 1) / rows);
     if (best < 0 || tiles < best) {  // equal tile counts -> equal waste; keep the wider tile
       best = tiles;
@@ -127,7 +127,7 @@ inline WtPlan wt_plan(const adct_geom& g) {
   }
   p.tpb = (int32_t)((W + p.tw - 1) / p.tw);
   p.tpi = (int32_t)(((H + p.rows - 1) / p.rows) * p.tpb);
-  p.cpi = (p.tpi + kWtChunkTiles - 1) / kWtChunkTiles;
+  p.cpi = (p.tpi + chunk_tiles - 1) / chunk_tiles;
   p.n_chunks = g.n_images * (int64_t)p.cpi;
   // tensor-map constraints: 16-byte aligned strides (< 2^40), dimensions < 2^32
   p.ok = (g.row_stride % 16) == 0 && (g.image_stride % 16) == 0 && g.image_stride < ((int64_t)1 << 40) &&
@@ -135,8 +135,59 @@ inline WtPlan wt_plan(const adct_geom& g) {
   return p;
 }
 
+inline WtPlan wt_plan(const adct_geom& g) { return tile_plan(g, kWtTileBytes, kWtChunkTiles); }
+
+// ---- tensor-core streaming kernel (fused_u8_tc_kernel, tc.cu; the default hot kernel) ----------
+// One persistent CTA per SM, warp-specialized.  A tile is 128 blocks (8 KB of u8 pixels, one TMA
+// box of 256 B x 32 rows or 128 B x 64 rows) = one M = 128 MMA.  Warps 0-3 (one per TMEM lane
+// quarter) convert the tile's blocks to f16 (exact subnormals x * 2^-24) into one of kTcAStages A
+// stages in TMEM; lane 0 of warp 0 also issues the kind::f16 MMA against the constant matrix B
+// in shared memory (retained Y = T X T^T and the column butterflies s, t of X, exact in fp32)
+// into one of kTcDStages D stages, and the TMA loads of the kTcSlots-deep tile ring.  Warps
+// 4.. are epilogue warps, kTcEpi per lane quarter, taking the CTA's tiles round-robin: each
+// reads its 32 blocks' D rows, releases the stage, and runs the fp32 inverse and squared error.
+// Per-(chunk, slot, quarter) fp64 partials, slot = tile index in the chunk mod kTcEpi.
+#ifndef ADCT_TC_EPI
+#define ADCT_TC_EPI 3
+#endif
+constexpr int kTcEpi = ADCT_TC_EPI;                 // epilogue warps per lane quarter
+constexpr int kTcWarps = 4 * kTcEpi + 4 + 2;      // epilogue, converters, MMA issuer, TMA producer
+constexpr int kTcConv0 = 4 * kTcEpi;              // first converter warp (a multiple of 4)
+constexpr int kTcThreads = 32 * kTcWarps;
+constexpr int kTcTileBytes = 8192;
+#ifndef ADCT_TC_SLOTS
+#define ADCT_TC_SLOTS 12
+#endif
+constexpr int kTcSlots = ADCT_TC_SLOTS;  // TMA ring depth (tiles)
+#ifndef ADCT_TC_ASTAGES
+#define ADCT_TC_ASTAGES 2
+#endif
+constexpr int kTcAStages = ADCT_TC_ASTAGES;
+
+#ifndef ADCT_TC_DSTAGES
+#define ADCT_TC_DSTAGES 5
+#endif
+constexpr int kTcDStages = ADCT_TC_DSTAGES;
+#ifndef ADCT_TC_CHUNK
+#define ADCT_TC_CHUNK 16
+#endif
+constexpr int kTcChunkTiles = ADCT_TC_CHUNK;      // tiles per chunk
+constexpr int kTcPartials = 4 * kTcEpi;           // partials per chunk
+constexpr int kTcBBytes = 96 * 64 * 2;            // B: N <= 96 outputs x K = 64 f16
+constexpr int kTcBars = 2 * kTcSlots + kTcAStages + 2 * kTcDStages;
+static_assert(kTcAStages < kTcDStages, "converters wait on the D barrier of tile t - kTcAStages");
+constexpr size_t kTcSmem = (size_t)kTcSlots * kTcTileBytes + kTcBBytes + (size_t)kTcBars * 8 + 16 + 128;
+static_assert(kTcSmem <= 227 * 1024, "tensor-core kernel exceeds shared memory");
+inline WtPlan tc_plan(const adct_geom& g) { return tile_plan(g, kTcTileBytes, kTcChunkTiles); }
+
 inline int64_t stream_partials_per_image(const adct_geom& g) {
   int64_t best = 0;
+  for (int tw : {256, 128}) {  // either tensor-core tile shape may be used
+    const int64_t rows = kTcTileBytes / tw;
+    const int64_t tpi = ((g.width + tw - 1) / tw) * ((g.height + rows - 1) / rows);
+    const int64_t c = (tpi + kTcChunkTiles - 1) / kTcChunkTiles * kTcPartials;
+    if (c > best) best = c;
+  }
   for (int tw : {256, 128}) {  // either warp-tile shape may be used (runtime matrices: 256 only)
     const int64_t rows = kWtTileBytes / tw;
     const int64_t tpi = ((g.width + tw - 1) / tw) * ((g.height + rows - 1) / rows);

@@ -26,6 +26,30 @@ namespace adct {
 void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
                      int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st);
 
+bool make_u8_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int tw, int rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.width, (cuuint64_t)g.height, (cuuint64_t)g.n_images};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.row_stride,
+                                 (cuuint64_t)(g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride)};
+  const cuuint32_t box[3] = {(cuuint32_t)tw, (cuuint32_t)rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(src), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int g_sms_s = 0;
+int sms_s() {
+  if (!g_sms_s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms_s, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms_s <= 0) g_sms_s = 148;
+  }
+  return g_sms_s;
+}
+
 namespace {
 
 __host__ __device__ constexpr int popc64s(uint64_t v) {
@@ -330,39 +354,23 @@ __global__ void __launch_bounds__(kWtThreads, 1)
   }
 }
 
-bool make_u8_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int tw, int rows) {
-  auto enc = tmap_encoder();
-  if (!enc) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)g.width, (cuuint64_t)g.height, (cuuint64_t)g.n_images};
-  const cuuint64_t strides[2] = {(cuuint64_t)g.row_stride,
-                                 (cuuint64_t)(g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride)};
-  const cuuint32_t box[3] = {(cuuint32_t)tw, (cuuint32_t)rows, 1};
-  const cuuint32_t es[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(src), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-int g_sms_s = 0;
-int sms_s() {
-  if (!g_sms_s) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms_s, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms_s <= 0) g_sms_s = 148;
-  }
-  return g_sms_s;
-}
-
 template <class MP, int R, int TW>
 bool launch_wtile_rt(const CUtensorMap& map, const WtArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(fused_u8_wtile_kernel<MP, R, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kWtSmem);
-  });
-  if (attr_err != cudaSuccess) return false;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  // the shared-memory opt-in is a per-device function attribute: set it once per device
+  static std::mutex mu;
+  static bool done[64] = {};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return false;
+    if (!done[dev]) {
+      if (cudaFuncSetAttribute(fused_u8_wtile_kernel<MP, R, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kWtSmem) != cudaSuccess)
+        return false;
+      done[dev] = true;
+    }
+  }
   const int64_t grid = (int64_t)a.n_chunks < sms_s() ? (int64_t)a.n_chunks : sms_s();
   fused_u8_wtile_kernel<MP, R, TW><<<(unsigned)grid, kWtThreads, kWtSmem, st>>>(map, a, dm, partial, 0x47000000u);
   return true;
@@ -404,8 +412,18 @@ bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const 
 // The streaming path for (u8 source, integer matrix, no clip, one r); returns false when the
 // geometry or r is not covered (the caller then uses the generic fused kernels).
 // On success the per-image SSE is in sse[n_images] (finalize launched on st).
+bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
+                 double* partial, cudaStream_t st, adct_status* status);
+
+// ADCT_HOT=tc selects the tensor-core streaming kernel (tc.cu) instead of this file's SIMT one
+static const bool g_hot_simt = [] {
+  const char* e = std::getenv("ADCT_HOT");
+  return !(e && std::strcmp(e, "tc") == 0);
+}();
+
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
                      double* partial, cudaStream_t st, adct_status* status) {
+  if (!g_hot_simt && fused_u8_tc(m, src, g, r, sse, partial, st, status)) return true;
   {
     WtPlan p = wt_plan(g);
     if (!p.ok || g.n_images == 0 || !aligned(src, 16)) return false;
