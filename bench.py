@@ -542,7 +542,7 @@ def main():
                        "hbm_gbs_step": world * blocks_step_rank * 64 / (ms_step * 1e-3) / 1e9 / world},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "fused_u8_wtile_kernel<T1Mat,10> + finalize_kernel (luma plane, 66,355,200 blocks x 64 B)",
+                         "kernel": ("fused_u8_wtile_kernel<T1Mat,10> (SIMT)" if os.environ.get("ADCT_HOT") == "simt" else "fused_u8_tc_kernel<T1Mat,10> (tcgen05 kind::i8)") + " + finalize_kernel (luma plane, 66,355,200 blocks x 64 B)",
                          "kernel_ms": luma_ms},
             "clocks": clk.summary(),
             # the binding constraint of the hot kernel: one warp-instruction per

@@ -138,55 +138,57 @@ inline WtPlan tile_plan(const adct_geom& g, int tile_bytes, int chunk_tiles) {
 inline WtPlan wt_plan(const adct_geom& g) { return tile_plan(g, kWtTileBytes, kWtChunkTiles); }
 
 // ---- tensor-core streaming kernel (fused_u8_tc_kernel, tc.cu; the default hot kernel) ----------
-// One persistent CTA per SM, warp-specialized.  A tile is 128 blocks (8 KB of u8 pixels, one TMA
-// box of 256 B x 32 rows or 128 B x 64 rows) = one M = 128 MMA.  Warps 0-3 (one per TMEM lane
-// quarter) convert the tile's blocks to f16 (exact subnormals x * 2^-24) into one of kTcAStages A
-// stages in TMEM; lane 0 of warp 0 also issues the kind::f16 MMA against the constant matrix B
-// in shared memory (retained Y = T X T^T and the column butterflies s, t of X, exact in fp32)
-// into one of kTcDStages D stages, and the TMA loads of the kTcSlots-deep tile ring.  Warps
-// 4.. are epilogue warps, kTcEpi per lane quarter, taking the CTA's tiles round-robin: each
-// reads its 32 blocks' D rows, releases the stage, and runs the fp32 inverse and squared error.
-// Per-(chunk, slot, quarter) fp64 partials, slot = tile index in the chunk mod kTcEpi.
-#ifndef ADCT_TC_EPI
-#define ADCT_TC_EPI 3
+// One persistent CTA per SM, warp-specialized: kTcEpi epilogue warps per TMEM lane quarter,
+// kTcIssuers MMA-issuer warps (one per SM sub-partition: a tcgen05.mma issue waits for issue
+// slots its sub-partition's FP32 warps also want, so tiles rotate over issuers), one TMA producer.  A tile is 128 pixel pairs = 256 blocks (16 KB of u8:
+// CW 128-byte chunks x 16/CW bands), loaded by TMA straight into the canonical K-major layout of
+// the kind::i8 MMA's A operand; see tc.cu.
+// kTcWays = epilogue warps per lane quarter = TMEM D stages = MMA-issuer warps: tile t uses D
+// stage t % kTcWays, issuer warp t % kTcWays and epilogue warps t % kTcWays, so every mbarrier
+// has one waiting agent that waits for its phases in order (a parity wait can never alias a
+// phase two ahead) and the issuers sit on different SM sub-partitions.
+#ifndef ADCT_TC_WAYS
+#define ADCT_TC_WAYS 3
 #endif
-constexpr int kTcEpi = ADCT_TC_EPI;                 // epilogue warps per lane quarter
-constexpr int kTcWarps = 4 * kTcEpi + 4 + 2;      // epilogue, converters, MMA issuer, TMA producer
-constexpr int kTcConv0 = 4 * kTcEpi;              // first converter warp (a multiple of 4)
+constexpr int kTcWays = ADCT_TC_WAYS;
+constexpr int kTcEpi = kTcWays;                     // epilogue warps per lane quarter
+constexpr int kTcEpiWarps = 4 * kTcEpi;
+constexpr int kTcIssuers = kTcWays;                 // MMA-issuer warps
+constexpr int kTcWarps = kTcEpiWarps + kTcIssuers + 1;  // + the TMA producer
 constexpr int kTcThreads = 32 * kTcWarps;
-constexpr int kTcTileBytes = 8192;
+constexpr int kTcTileBytes = 16384;
 #ifndef ADCT_TC_SLOTS
 #define ADCT_TC_SLOTS 12
 #endif
-constexpr int kTcSlots = ADCT_TC_SLOTS;  // TMA ring depth (tiles)
-#ifndef ADCT_TC_ASTAGES
-#define ADCT_TC_ASTAGES 2
-#endif
-constexpr int kTcAStages = ADCT_TC_ASTAGES;
-
-#ifndef ADCT_TC_DSTAGES
-#define ADCT_TC_DSTAGES 5
-#endif
-constexpr int kTcDStages = ADCT_TC_DSTAGES;
+constexpr int kTcSlots = ADCT_TC_SLOTS;  // pixel-tile ring depth
+static_assert(kTcSlots % kTcWays == 0, "slot s only ever holds tiles of issuer s % kTcWays");
+constexpr int kTcDStages = kTcWays;               // TMEM accumulator stages (N <= 160 columns each)
 #ifndef ADCT_TC_CHUNK
-#define ADCT_TC_CHUNK 16
+#define ADCT_TC_CHUNK 24
 #endif
 constexpr int kTcChunkTiles = ADCT_TC_CHUNK;      // tiles per chunk
 constexpr int kTcPartials = 4 * kTcEpi;           // partials per chunk
-constexpr int kTcBBytes = 96 * 64 * 2;            // B: N <= 96 outputs x K = 64 f16
-constexpr int kTcBars = 2 * kTcSlots + kTcAStages + 2 * kTcDStages;
-static_assert(kTcAStages < kTcDStages, "converters wait on the D barrier of tile t - kTcAStages");
-constexpr size_t kTcSmem = (size_t)kTcSlots * kTcTileBytes + kTcBBytes + (size_t)kTcBars * 8 + 16 + 128;
+constexpr int kTcBBytes = 160 * 128;              // B: N <= 160 outputs x K = 128 s8
+constexpr int kTcBars = 2 * kTcSlots + 4 * kTcDStages;
+constexpr size_t kTcSmem = (size_t)kTcSlots * kTcTileBytes + kTcBBytes + (size_t)kTcBars * 8 + 16 + 1024;
 static_assert(kTcSmem <= 227 * 1024, "tensor-core kernel exceeds shared memory");
-inline WtPlan tc_plan(const adct_geom& g) { return tile_plan(g, kTcTileBytes, kTcChunkTiles); }
+struct TcPlan {
+  int32_t cw;        // tile width in 128-byte chunks (16 / cw bands high)
+  int32_t tpr, tpi;  // tiles per tile row, per image
+  int32_t cpi;       // chunks per image
+  int64_t n_chunks;
+  bool ok;
+};
+TcPlan tc_plan(const adct_geom& g);  // tc.cu
 
 inline int64_t stream_partials_per_image(const adct_geom& g) {
   int64_t best = 0;
-  for (int tw : {256, 128}) {  // either tensor-core tile shape may be used
-    const int64_t rows = kTcTileBytes / tw;
-    const int64_t tpi = ((g.width + tw - 1) / tw) * ((g.height + rows - 1) / rows);
-    const int64_t c = (tpi + kTcChunkTiles - 1) / kTcChunkTiles * kTcPartials;
-    if (c > best) best = c;
+  if (g.width % 128 == 0) {  // tensor-core tiles (any of its shapes)
+    for (int cw : {16, 2, 1}) {
+      const int64_t tpi = ((g.width / 128 + cw - 1) / cw) * ((g.height / 8 + 16 / cw - 1) / (16 / cw));
+      const int64_t c = (tpi + kTcChunkTiles - 1) / kTcChunkTiles * kTcPartials;
+      if (c > best) best = c;
+    }
   }
   for (int tw : {256, 128}) {  // either warp-tile shape may be used (runtime matrices: 256 only)
     const int64_t rows = kWtTileBytes / tw;

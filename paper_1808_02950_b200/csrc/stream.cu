@@ -415,10 +415,11 @@ bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const 
 bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
                  double* partial, cudaStream_t st, adct_status* status);
 
-// ADCT_HOT=tc selects the tensor-core streaming kernel (tc.cu) instead of this file's SIMT one
+// ADCT_HOT=simt selects this file's SIMT streaming kernel instead of the tensor-core one (tc.cu;
+// A/B runs and the SIMT parity tests)
 static const bool g_hot_simt = [] {
   const char* e = std::getenv("ADCT_HOT");
-  return !(e && std::strcmp(e, "tc") == 0);
+  return e && std::strcmp(e, "simt") == 0;
 }();
 
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,

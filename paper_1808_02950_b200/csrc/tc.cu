@@ -1,31 +1,39 @@
 // tc.cu — the tensor-core hot kernel of BASELINE.json config 4: forward -> zonal retention ->
 // inverse -> squared error per image (§6.1) for uint8 planes, every 8x8
-// block read from HBM exactly once (TMA tile rings), the linear part of the forward on tcgen05.
+// block read from HBM exactly once, the forward's dense contraction on tcgen05 (kind::i8).
 //
-// Per block x (64 samples, k = 8i + j) the tensor core computes, exactly, the outputs
-//   Y_kl = sum_ij T_ki T_lj x_ij     for the retained (k,l)          (Eq. 1)
-//   s_i[j] = x_ij + x_(7-i)j,  t_i[j] = x_ij - x_(7-i)j   (i < 4)     (first column butterfly)
-// as D = A B^T with A = the block as f16 (one row of the M = 128 tile per block; a u8 sample x
-// is the f16 SUBNORMAL x * 2^-24, built by one PRMT per two samples) and B = the constant
-// [outputs x 64] matrix of those coefficients (integers |b| <= 4, exact in f16).  Products and
-// partial sums are integers times 2^-24 below 2^24 * 2^-24, so the fp32 accumulators hold the
-// exact integer results scaled by 2^-24 (probes/tc_probe.cu).  The thread that owns the block
-// then runs the same fp32 arithmetic as the SIMT kernel (stream.cu, block_sse_u8s): weights
+// Operand A is the raw pixel tile exactly as TMA lands it.  A 5-D tensor map over the u8 plane
+// with dims {128 bytes, 8 rows, bands, 128-byte chunks, images} and strides {row, 8 rows, 128 B,
+// image} (non-monotonic, accepted by the driver; probes/i8_probe.cu) places a box
+// {128, 8, BH, CW, 1} (CW chunks x BH bands, CW * BH = 16) in shared memory as
+// [chunk][band][row][128 B]: the canonical K-major no-swizzle layout of A = [pair p][k] with
+// row p = two horizontally adjacent blocks (16 bytes of each of their 8 rows, k = 16 i + c),
+// 8-pair groups 1024 B apart (SBO) and pixel rows 128 B apart (LBO).  So M = 128 pairs = 256
+// blocks per tile, K = 128 u8 samples per pair, and no thread touches the pixels.
+//
+// Operand B (shared memory, s8) is the constant block-diagonal [2 NB x 128] matrix that gives,
+// per block, exactly (Eq. 1):
+//   Y_kl = sum_ij T_ki T_lj x_ij     for the coefficients the inverse needs (retained; for
+//                                    r > 32 the dropped ones, reading A17)
+//   s_i[j] = x_ij + x_(7-i)j,  t_i[j] = x_ij - x_(7-i)j   (i < 4, the first column butterfly)
+// |b| <= 4, products and sums are exact in the s32 TMEM accumulators.  D column n of lane p:
+// block 2p + n / NB, output n % NB.  4 MMAs of K = 32 per 256 blocks.
+//
+// The epilogue thread that owns lane p converts its two blocks' outputs to fp32 (exact) and
+// runs the same fp32 arithmetic as the SIMT kernel (stream.cu, block_sse_u8s): weights
 // 2/(n_k n_l), the horizontal inverse Q = (W o Y') T of the retained rows, and the vertical
 // inverse fused with the error, (x_i - x^_i)^2 + (x_7-i - x^_7-i)^2 = ((s_i - 2E_i)^2 +
-// (t_i - 2O_i)^2)/2.  Every fp32 value carries the exact factor 2^-24 (no subnormal occurs), so
-// the per-block SSE is 2^-48 times that of the SIMT kernel bit for bit; the fp64 partial
-// removes the factor exactly.  For r > 32 the inverse of the dropped coefficients is formed
-// (exactly 0 at r = 64; reading A17) and s, t are not needed.
+// (t_i - 2O_i)^2)/2; for r > 32 the inverse of the dropped coefficients is x - x^ itself.
 //
-// Roles inside a persistent CTA (one per SM): kTcGroups groups of 4 warps; warp q of a group
-// reads TMEM lanes 32q..32q+31.  Per group and tile: one lane issues the TMA load of the 8 KB
-// tile (kTcSlots-deep ring), every thread converts its block and tcgen05.st's it into the
-// group's A columns, a named barrier joins the 4 warps, one lane issues 4 MMAs (K = 64) and
-// commits to the group's mbarrier, and every thread tcgen05.ld's its block's outputs.  Groups
-// never wait for each other, so the SM's issue slots stay busy while one group waits for its
-// MMA.  DESIGN.md §5.2.
-#include <cuda_fp16.h>
+// Warp roles of the persistent CTA (one per SM): kTcEpi epilogue warps per TMEM
+// lane quarter (tiles round-robin), kTcIssuers MMA-issuer warps (one per SM sub-partition, tiles
+// round-robin: a tcgen05.mma waits for its sub-partition's issue slots, which the FP32 epilogue
+// saturates, so one issuer alone would pace the kernel; probes/tc_contend.cu), one TMA producer.  Rings: kTcSlots
+// pixel tiles in shared memory (refilled when the tile's MMA has completed), kTcDStages D stages
+// in TMEM (released by the epilogue warps once their tcgen05.ld completed).  Deterministic fp64
+// partials per (chunk, tile index in the chunk mod kTcEpi, lane quarter).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -38,7 +46,6 @@ namespace adct {
 
 void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
                      int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st);
-bool make_u8_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int tw, int rows);
 int sms_s();
 
 namespace {
@@ -63,10 +70,11 @@ struct TcShape {
   static constexpr uint64_t NZ = RESID ? ~KEEP : KEEP;  // coefficients the inverse uses
   static constexpr int NNZ = popc64t(NZ);
   static constexpr int NY = (NNZ + 15) / 16 * 16;       // coefficient columns (x16 loads)
-  static constexpr int N = NY + (RESID ? 0 : 64);       // + s_i[j], t_i[j]: column NY + 8j + i (+4 for t)
+  static constexpr int NB = NY + (RESID ? 0 : 64);      // per block: + s_i[j] at NY + 8j + i, t_i[j] at +4
+  static constexpr int N = 2 * NB;                      // MMA N: the pair's two blocks
   static constexpr uint32_t ROWS = row_mask_t(NZ);
-  static_assert(NNZ <= 32, "at most 32 coefficient columns");
-  static_assert(N <= 96, "TMEM budget: kTcGroups x (N + 32) <= 512 columns");
+  static_assert(NNZ >= 1 && NNZ <= 32, "1..32 coefficient columns");
+  static_assert(N <= 256 && N % 16 == 0, "MMA N");
 };
 
 // index of coefficient p = k*8+l among the set bits of NZ (its D column)
@@ -75,71 +83,68 @@ __host__ __device__ constexpr int nz_index(int p) {
   return popc64t(NZ & ((p == 0) ? 0ull : (~0ull >> (64 - p))));
 }
 
-// ---- one block from its D row (in registers): the fp32 inverse and squared error ------------
-// yr: the NY coefficient columns; st: s_i[j] at 8j + i, t_i[j] at 8j + 4 + i.  Returns 2^-48 x SSE.
+__device__ __forceinline__ float i2f(uint32_t v) { return __int2float_rn((int32_t)v); }  // exact, |v| < 2^24
+
+// ---- one block from its D row (s32 in registers): fp32 inverse and squared error ------------
+// yr: the NY coefficient columns; st: s_i[j] at 8j + i, t_i[j] at 8j + 4 + i (unused for r > 32)
 template <class MP, int R>
 __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, const uint32_t* st) {
   using S = TcShape<R>;
   constexpr uint64_t NZ = S::NZ;
   constexpr uint32_t ROWS = S::ROWS;
-  if constexpr (S::NNZ == 0) {
-    return 0.0f;  // r = 64
-  } else {
-    // horizontal inverse of the weighted retained coefficients, Q = (W o Y') T, rows in ROWS
-    float q[8][8];
+  // horizontal inverse of the weighted coefficients, Q = (W o Y') T, rows in ROWS
+  float q[8][8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (!((ROWS >> k) & 1u)) continue;
-      float z[8];
+  for (int k = 0; k < 8; ++k) {
+    if (!((ROWS >> k) & 1u)) continue;
+    float z[8];
 #pragma unroll
-      for (int l = 0; l < 8; ++l)
-        z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? __uint_as_float(yr[nz_index<NZ>(k * 8 + l)]) * m.wy2(k, l) : 0.0f;
+    for (int l = 0; l < 8; ++l)
+      z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? i2f(yr[nz_index<NZ>(k * 8 + l)]) * m.wy2(k, l) : 0.0f;
 #define ADCT_TC_ROWINV(K)                                              \
   if (k == K) {                                                        \
     constexpr uint32_t rm = (uint32_t)((NZ >> (8 * K)) & 0xffull);     \
     if constexpr (rm != 0) inv8<MP, rm>(m, z, q[K]);                   \
   }
-      ADCT_TC_ROWINV(0) ADCT_TC_ROWINV(1) ADCT_TC_ROWINV(2) ADCT_TC_ROWINV(3)
-      ADCT_TC_ROWINV(4) ADCT_TC_ROWINV(5) ADCT_TC_ROWINV(6) ADCT_TC_ROWINV(7)
+    ADCT_TC_ROWINV(0) ADCT_TC_ROWINV(1) ADCT_TC_ROWINV(2) ADCT_TC_ROWINV(3)
+    ADCT_TC_ROWINV(4) ADCT_TC_ROWINV(5) ADCT_TC_ROWINV(6) ADCT_TC_ROWINV(7)
 #undef ADCT_TC_ROWINV
-    }
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  }
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float col[8];
+  for (int j = 0; j < 8; ++j) {
+    float col[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) col[k] = ((ROWS >> k) & 1u) ? q[k][j] : 0.0f;
-      if constexpr (S::RESID) {  // x - x^ = inverse of the dropped coefficients
-        float e[4], o[4];
-        inv8_eo<MP, ROWS>(m, col, e, o);
+    for (int k = 0; k < 8; ++k) col[k] = ((ROWS >> k) & 1u) ? q[k][j] : 0.0f;
+    if constexpr (S::RESID) {  // x - x^ = inverse of the dropped coefficients
+      float e[4], o[4];
+      inv8_eo<MP, ROWS>(m, col, e, o);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc[i] = fmaf(e[i], e[i], acc[i]);
-          acc[i] = fmaf(o[i], o[i], acc[i]);
-        }
-      } else {
-        float e[4];
-        inv8_e<MP, ROWS>(m, col, e);
+      for (int i = 0; i < 4; ++i) {
+        acc[i] = fmaf(e[i], e[i], acc[i]);
+        acc[i] = fmaf(o[i], o[i], acc[i]);
+      }
+    } else {
+      float e[4];
+      inv8_e<MP, ROWS>(m, col, e);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float dp = __uint_as_float(st[8 * j + i]) - e[i];
-          const float dm =
-              lsub<MP, 8, ROWS & 0xaau>(__uint_as_float(st[8 * j + 4 + i]), [&](int k) { return m.h(i, k); }, col);
-          acc[i] = fmaf(dp, dp, acc[i]);
-          acc[i] = fmaf(dm, dm, acc[i]);
-        }
+      for (int i = 0; i < 4; ++i) {
+        const float dp = i2f(st[8 * j + i]) - e[i];
+        const float dm = lsub<MP, 8, ROWS & 0xaau>(i2f(st[8 * j + 4 + i]), [&](int k) { return m.h(i, k); }, col);
+        acc[i] = fmaf(dp, dp, acc[i]);
+        acc[i] = fmaf(dm, dm, acc[i]);
       }
     }
-    return 0.5f * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
   }
+  return 0.5f * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
 }
 
 // ---- the CTA's tiles: chunks cg = blockIdx.x, +gridDim.x, ...; a chunk is kTcChunkTiles
 // consecutive tiles of one image (fewer at the image's end), taken in order ------------------
 struct TcArgs {
-  int32_t tpb, tpi, cpi;
+  int32_t tpr, tpi, cpi;  // tiles per tile row, per image; chunks per image
   uint32_t n_chunks;
-  FastDiv dcpi, dtpb;
+  FastDiv dcpi, dtpr;
 };
 
 __device__ __forceinline__ int32_t chunk_tiles(const TcArgs& a, uint32_t cg, uint32_t& img, int32_t& tt0) {
@@ -148,23 +153,23 @@ __device__ __forceinline__ int32_t chunk_tiles(const TcArgs& a, uint32_t cg, uin
   return min(kTcChunkTiles, a.tpi - tt0);
 }
 
-struct TcPf {  // the TMA issuer's walk: coordinates of the next tile to load
+struct TcPf {  // the TMA producer's walk: coordinates of the next tile to load
   uint32_t cg, img;
-  int32_t j, n, pair, slice;
+  int32_t j, n, trow, tcol;
 };
 __device__ __forceinline__ void pf_enter(const TcArgs& a, TcPf& f) {
   if (f.cg >= a.n_chunks) return;
   int32_t tt0;
   f.n = chunk_tiles(a, f.cg, f.img, tt0);
   f.j = 0;
-  f.pair = (int32_t)fdiv((uint32_t)tt0, a.dtpb);
-  f.slice = tt0 - f.pair * a.tpb;
+  f.trow = (int32_t)fdiv((uint32_t)tt0, a.dtpr);
+  f.tcol = tt0 - f.trow * a.tpr;
 }
 __device__ __forceinline__ void pf_next(const TcArgs& a, TcPf& f) {
   if (++f.j < f.n) {
-    if (++f.slice == a.tpb) {
-      f.slice = 0;
-      ++f.pair;
+    if (++f.tcol == a.tpr) {
+      f.tcol = 0;
+      ++f.trow;
     }
   } else {
     f.cg += gridDim.x;
@@ -172,73 +177,76 @@ __device__ __forceinline__ void pf_next(const TcArgs& a, TcPf& f) {
   }
 }
 
-// B[n][k] of the MMA (row n = output, k = 8i + j), integers |b| <= 4
-template <class MP, int R>
-__device__ __forceinline__ float tc_bval(const MP& m, int n, int k) {
-  using S = TcShape<R>;
-  const int i = k >> 3, j = k & 7;
-  if (n < S::NNZ) {
-    int p = 0, c = -1;
-    for (; p < 64; ++p)
-      if ((S::NZ >> p) & 1ull)
-        if (++c == n) break;
-    return m.f(p >> 3, i) * m.f(p & 7, j);
-  }
-  if (n < S::NY) return 0.0f;
-  const int jj = (n - S::NY) >> 3, r = (n - S::NY) & 7;
-  if (j != jj) return 0.0f;
-  if (r < 4) return (i == r || i == 7 - r) ? 1.0f : 0.0f;       // s_r[j]
-  return i == r - 4 ? 1.0f : (i == 11 - r ? -1.0f : 0.0f);      // t_(r-4)[j]
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                            int32_t c3, int32_t c4, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
 }
 
-template <class MP, int R, int TW>
+template <class MP, int R, int CW>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    fused_u8_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a, DevMat dm, double* __restrict__ partial,
-                       long long* __restrict__ trace) {
-  // trace (debug builds with ADCT_TC_TRACE): clock64 stamps of CTA 0's first kTrTiles tiles
-  constexpr int kTrTiles = 64;
-#ifdef ADCT_TC_TRACE
-#define TR(slot, tile) \
-  { if (trace && blockIdx.x == 0 && (tile) < kTrTiles && lane == 0) trace[(tile) * 16 + (slot)] = clock64(); }
-#else
-#define TR(slot, tile) {}
-#endif
+    fused_u8_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a, DevMat dm, double* __restrict__ partial) {
   using S = TcShape<R>;
-  constexpr int N = S::N;
-  constexpr int RT = kTcTileBytes / TW;  // rows per tile
-  constexpr int BPR = TW / 8;            // blocks per band in a tile
-  constexpr uint32_t kIdesc = idesc_f16_f32<128, N>();
+  constexpr int N = S::N, NB = S::NB;
+  constexpr int BH = 16 / CW;  // bands per tile
+  // kind::i8: D s32 (2 << 4), A u8 (0 << 7), B s8 (1 << 10), both K-major, N >> 3, M >> 4
+  // each tile is two MMA sets of N = NB (half h: block 2p + h of every pair), each into its own
+  // TMEM half-stage, so an epilogue warp releases block 2p's columns before it computes
+  constexpr uint32_t kIdesc = (2u << 4) | (1u << 10) | ((uint32_t)(NB >> 3) << 17) | (8u << 24);
   constexpr uint32_t kTmemCols = 512;
-  constexpr uint32_t kACol0 = (uint32_t)(kTcDStages * N);  // A stages after the D stages
-  static_assert(kTcDStages * N + kTcAStages * 32 <= (int)kTmemCols, "TMEM columns");
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+  static_assert(2 * kTcDStages * NB <= (int)kTmemCols, "TMEM columns");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = w & 3;  // TMEM lane quarter of this warp (hardware: warp w accesses lanes 32 (w % 4) ..)
   uint8_t* sB = smem + (size_t)kTcSlots * kTcTileBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kTcBBytes);  // [kTcSlots]  TMA tile landed
-  uint64_t* afull = full + kTcSlots;                              // [2]  A stage written (4 warps)
-  uint64_t* dfull = afull + kTcAStages;                           // [D]  MMA of the tile done (commit)
-  uint64_t* dfree = dfull + kTcDStages;                           // [D]  D read by the 4 epilogue warps
-  uint64_t* sfree = dfree + kTcDStages;                           // [kTcSlots]  slot read by the 4 converters
-  uint32_t* holder = reinterpret_cast<uint32_t*>(sfree + kTcSlots);
+  uint64_t* sfree = full + kTcSlots;                              // [kTcSlots]  MMA done reading the tile
+  uint64_t* dfull = sfree + kTcSlots;                             // [2D] MMA done writing a half-stage
+  uint64_t* dfree = dfull + 2 * kTcDStages;                       // [2D] half-stage read by 4 epilogue warps
+  uint32_t* holder = reinterpret_cast<uint32_t*>(dfree + 2 * kTcDStages);
   const MP m(dm);
 
-  // B in the canonical K-major no-swizzle layout: core matrix (n/8, k/8) at (n/8)*1024 + (k/8)*128
-  for (int idx = threadIdx.x; idx < N * 64; idx += kTcThreads) {
-    const int n = idx >> 6, k = idx & 63;
-    const __half h = __float2half_rn(tc_bval<MP, R>(m, n, k));
-    *reinterpret_cast<__half*>(sB + (n >> 3) * 1024 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2) = h;
+  // B in the canonical K-major no-swizzle layout: core matrix (n/8, k/16) at (n/8)*1024 + (k/16)*128;
+  // thread n writes row n, one 16-byte pixel row i (both blocks) at a time
+  for (int n = threadIdx.x; n < N; n += kTcThreads) {
+    const int blk = n / NB, o = n % NB;
+    int pk = -1, pl = -1, sj = -1, sr = -1;
+    if (o < S::NNZ) {
+      int cnt = -1;
+      for (int p = 0; p < 64; ++p)
+        if (((S::NZ >> p) & 1ull) && ++cnt == o) {
+          pk = p >> 3;
+          pl = p & 7;
+          break;
+        }
+    } else if (o >= S::NY) {
+      sj = (o - S::NY) >> 3;  // column j of s_r / t_(r-4)
+      sr = (o - S::NY) & 7;
+    }
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) {
+      uint32_t wv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int v = 0;
+        if (pk >= 0) v = (int)lrintf(m.f(pk, i) * m.f(pl, j));
+        else if (sj == j) v = sr < 4 ? ((i == sr || i == 7 - sr) ? 1 : 0) : (i == sr - 4 ? 1 : (i == 11 - sr ? -1 : 0));
+        const int c = 8 * blk + j;  // byte of the 16-byte pixel row of the pair
+        wv[c >> 2] |= ((uint32_t)(uint8_t)(int8_t)v) << (8 * (c & 3));
+      }
+      *reinterpret_cast<uint4*>(sB + (n >> 3) * 1024 + i * 128 + (n & 7) * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kTcSlots; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&sfree[i], 4);
+      mbar_init(&sfree[i], 1);
     }
-    for (int i = 0; i < kTcAStages; ++i) {
-      mbar_init(&afull[i], 4);
-    }
-    for (int i = 0; i < kTcDStages; ++i) {
+    for (int i = 0; i < 2 * kTcDStages; ++i) {
       mbar_init(&dfull[i], 1);
       mbar_init(&dfree[i], 4);
     }
@@ -250,23 +258,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *holder;
-  const uint32_t lane_q = (uint32_t)(32 * q) << 16;
   const uint32_t full0 = smem_u32(full), ring0 = smem_u32(smem), sB_u = smem_u32(sB);
 
-  if (w == kTcConv0 + 5) {
-    // ======== TMA producer: a slot is refilled once every quarter has converted its tile ========
+  if (w == kTcEpiWarps + kTcIssuers) {
+    // ======== TMA producer: one 16 KB tile per slot, refilled when its MMA has completed ========
     TcPf pf;
     pf.cg = blockIdx.x;
     pf_enter(a, pf);
     uint32_t slot = 0, sph = 0, t = 0;
 #pragma unroll 1
     for (; pf.cg < a.n_chunks; ++t) {
-      if (t >= (uint32_t)kTcSlots) mbar_wait(&sfree[slot], sph ^ 1u);  // tile t - kTcSlots read by all 4 quarters
+      if (t >= (uint32_t)kTcSlots) mbar_wait_sleep(&sfree[slot], sph ^ 1u);  // MMA of tile t - kTcSlots done
       if (elect_one()) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + slot * 8),
                      "r"((uint32_t)kTcTileBytes)
                      : "memory");
-        tma_load_3d(ring0 + slot * kTcTileBytes, &tmap, pf.slice * TW, pf.pair * RT, (int32_t)pf.img,
+        tma_load_5d(ring0 + slot * kTcTileBytes, &tmap, 0, 0, pf.trow * BH, pf.tcol * CW, (int32_t)pf.img,
                     full0 + slot * 8);
       }
       __syncwarp();
@@ -276,104 +283,47 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         sph ^= 1u;
       }
     }
-  } else if (w == kTcConv0 + 4) {
-    // ======== MMA issuer: one elected lane issues every tile's MMA ========
-    uint32_t ds = 0, dph = 0, as = 0, aph = 0, t = 0;
+  } else if (w >= kTcEpiWarps) {
+    // ======== MMA issuers: warp kTcEpiWarps + i issues the 4 MMAs of the tiles t = i (mod kTcIssuers) ========
+    const uint32_t iss = (uint32_t)(w - kTcEpiWarps);
+    // descriptors of slot 0 / k-step 0: the others differ only in the start address (bits 0-13)
+    const uint64_t adesc0 = smem_desc_kmajor(ring0, 128, 1024), bdesc0 = smem_desc_kmajor(sB_u, 128, 1024);
+    uint32_t t = 0;
 #pragma unroll 1
     for (uint32_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
       uint32_t img;
       int32_t tt0;
       const int32_t n = chunk_tiles(a, cg, img, tt0);
+      const int32_t j0 = (int32_t)((iss + kTcIssuers - t % kTcIssuers) % kTcIssuers);
 #pragma unroll 1
-      for (int32_t j = 0; j < n; ++j, ++t) {
-        TR(4, t)
-        mbar_wait(&afull[as], aph);                                      // all 4 quarters of A written
-        TR(5, t)
-        if (t >= (uint32_t)kTcDStages) mbar_wait(&dfree[ds], dph ^ 1u);  // tile t - D read by the epilogue
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t tDs = tbase + (uint32_t)(N * ds), tAs = tbase + kACol0 + 32 * as;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_f16_ts(tDs, tAs + 8 * kk, smem_desc_kmajor(sB_u + kk * 256, 128, 1024), kIdesc, kk > 0 ? 1u : 0u);
-          mma_commit(smem_u32(&dfull[ds]));  // D of tile t written (A of tile t free again)
-        }
-        __syncwarp();
-        TR(6, t)
-        if (++ds == kTcDStages) {
-          ds = 0;
-          dph ^= 1u;
-        }
-        if (++as == (uint32_t)kTcAStages) {
-          as = 0;
-          aph ^= 1u;
-        }
-      }
-    }
-  } else if (w >= kTcConv0) {
-    // ======== converters (warps kTcConv0 .. +3, one per TMEM lane quarter) ========
-    // the thread's block in a tile: band (q or 2q + lane/16) and column, rows at stride TW
-    const int band = (BPR == 32) ? q : 2 * q + (lane >> 4);
-    const uint32_t my_off = (uint32_t)(band * 8 * TW + (lane % BPR) * 8);
-    uint32_t slot = 0, phase = 0, as = 0, aph = 0, t = 0;
-#pragma unroll 1
-    for (uint32_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
-      uint32_t img;
-      int32_t tt0;
-      const int32_t n = chunk_tiles(a, cg, img, tt0);
-#pragma unroll 1
-      for (int32_t j = 0; j < n; ++j, ++t) {
-        if (q == 1) TR(0, t)
-        if (t >= (uint32_t)kTcAStages) {  // the MMA of tile t - A (the last reader of A[as]) has completed
-          const uint32_t tp = t - kTcAStages;
-          mbar_wait(&dfull[tp % kTcDStages], (tp / kTcDStages) & 1u);
-        }
-        if (q == 1) TR(1, t)
-        mbar_wait(&full[slot], phase);
-        if (q == 1) TR(2, t)
-        const uint32_t p = ring0 + slot * kTcTileBytes + my_off;
-        const uint32_t tA = tbase + lane_q + kACol0 + 32 * as;
+      for (int32_t j = j0; j < n; j += kTcIssuers) {
+        const uint32_t tt = t + (uint32_t)j;
+        const uint32_t slot = tt % kTcSlots, ds = tt % kTcDStages, dpar = ((tt / kTcDStages) & 1u) ^ 1u;
+        mbar_wait_sleep(&full[slot], (tt / kTcSlots) & 1u);  // pixels landed
+        const uint64_t ad = adesc0 + (uint64_t)(slot * (kTcTileBytes >> 4));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          uint32_t av[16];
+          const uint32_t hs = 2 * ds + (uint32_t)h;
+          if (tt >= (uint32_t)kTcDStages) mbar_wait_sleep(&dfree[hs], dpar);  // tile tt - D's half h read
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t td = tbase + (uint32_t)NB * hs;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const uint2 r = lds64(p + (uint32_t)((4 * h + i) * TW));
-            // f16x2 subnormals {x_2c, x_2c+1} * 2^-24: bytes [x, 0, x', 0]
-            asm("prmt.b32 %0, %1, 0, 0x4140;" : "=r"(av[4 * i + 0]) : "r"(r.x));
-            asm("prmt.b32 %0, %1, 0, 0x4342;" : "=r"(av[4 * i + 1]) : "r"(r.x));
-            asm("prmt.b32 %0, %1, 0, 0x4140;" : "=r"(av[4 * i + 2]) : "r"(r.y));
-            asm("prmt.b32 %0, %1, 0, 0x4342;" : "=r"(av[4 * i + 3]) : "r"(r.y));
+            for (int kk = 0; kk < 4; ++kk)
+              mma_i8_ss(td, ad + (uint64_t)(kk * 16), bdesc0 + (uint64_t)(h * (NB / 8) * 64 + kk * 16), kIdesc,
+                        kk > 0 ? 1u : 0u);
+            mma_commit(smem_u32(&dfull[hs]));                // half h of tile tt written
+            if (h == 1) mma_commit(smem_u32(&sfree[slot]));  // the slot may be refilled
           }
-#ifndef ADCT_TC_ABL_NOSTTM
-          tmem_st16(tA + 16 * h, av);
-#else
-          if (av[0] == 0x12345u && av[15] == 7u) tmem_st16(tA + 16 * h, av);
-#endif
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&sfree[slot]);  // the producer may refill the slot
-          mbar_arrive(&afull[as]);    // the issuer may run the MMA
-        }
-        if (q == 1) TR(3, t)
-        if (++slot == kTcSlots) {
-          slot = 0;
-          phase ^= 1u;
-        }
-        if (++as == (uint32_t)kTcAStages) {
-          as = 0;
-          aph ^= 1u;
+          __syncwarp();
         }
       }
+      t += (uint32_t)n;
     }
   } else {
     // ======== epilogue warps: quarter q, index e; tiles t = e, e + kTcEpi, ... of the CTA ========
     const int e = w >> 2;
-    uint32_t yr[S::NY], st[64];
-    (void)st;
+    const uint32_t lane_q = (uint32_t)(32 * q) << 16;
     uint32_t t = 0;
 #pragma unroll 1
     for (uint32_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
@@ -387,52 +337,42 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll 1
       for (int32_t j = sl; j < n; j += kTcEpi) {
         const uint32_t tt = t + (uint32_t)j;
-        const uint32_t d = tt % kTcDStages;
-        if (q == 0) TR(8, tt)
-        mbar_wait(&dfull[d], (tt / kTcDStages) & 1u);
-        if (q == 0) TR(9, tt)
-        tc_fence_after();
-        const uint32_t tD = tbase + lane_q + (uint32_t)(N * d);
-#ifdef ADCT_TC_ABL_NOLDTM
-        if (tt == 0xffffffffu)
-#endif
-        if constexpr (S::NY == 16) tmem_ld16(tD, yr);
-        else tmem_ld32(tD, yr);
-#ifdef ADCT_TC_ABL_NOLDTM
-        if (tt == 0xffffffffu)
-#endif
-        if constexpr (!S::RESID) {
-          tmem_ld32(tD + S::NY, *reinterpret_cast<uint32_t(*)[32]>(&st[0]));
-          tmem_ld32(tD + S::NY + 32, *reinterpret_cast<uint32_t(*)[32]>(&st[32]));
+        const uint32_t d = tt % kTcDStages, dpar = (tt / kTcDStages) & 1u;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // block 2p + h from half-stage 2d + h
+          const uint32_t hs = 2 * d + (uint32_t)h;
+          mbar_wait_sleep(&dfull[hs], dpar);
+          tc_fence_after();
+          const uint32_t tD = tbase + lane_q + (uint32_t)(NB * hs);
+          uint32_t yr[S::NY], st[64];
+          if constexpr (S::NY == 16) tmem_ld16(tD, yr);
+          else tmem_ld32(tD, yr);
+          if constexpr (!S::RESID) {
+            tmem_ld32(tD + S::NY, *reinterpret_cast<uint32_t(*)[32]>(&st[0]));
+            tmem_ld32(tD + S::NY + 32, *reinterpret_cast<uint32_t(*)[32]>(&st[32]));
+          }
+          tmem_wait_ld(yr);
+          if constexpr (!S::RESID) tmem_wait_ld(st);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dfree[hs]);  // the MMA of tile tt + D may overwrite the half-stage
+          acc += tc_block_sse<MP, R>(m, yr, st);
         }
-        tmem_wait_ld(yr);
-        if constexpr (!S::RESID) tmem_wait_ld(st);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&dfree[d]);  // the MMA of tile tt + D may overwrite the stage
-        if (q == 0) TR(10, tt)
-#ifndef ADCT_TC_ABL_NOEPI
-        acc += tc_block_sse<MP, R>(m, yr, st);
-#else
-        acc += __uint_as_float(yr[0]);
-#endif
-        if (q == 0) TR(11, tt)
       }
-      double v = (double)acc;
+      float v = acc;  // fixed shuffle order: the partial depends on the geometry only
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) partial[((int64_t)cg * kTcEpi + sl) * 4 + q] = v * 0x1p48;  // remove 2^-48
+      if (lane == 0) partial[((int64_t)cg * kTcEpi + sl) * 4 + q] = (double)v;
       t += (uint32_t)n;
     }
   }
   tc_fence_before();
   __syncthreads();
   if (w == 0) tmem_dealloc<kTmemCols>(tbase);
-#undef TR
 }
 
-template <class MP, int R, int TW>
-bool launch_tc_rt(const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
+template <class MP, int R, int CW>
+bool launch_tc_rc(const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   // the shared-memory opt-in is a per-device function attribute: set it once per device
@@ -442,81 +382,104 @@ bool launch_tc_rt(const CUtensorMap& map, const TcArgs& a, const DevMat& dm, dou
     std::lock_guard<std::mutex> lk(mu);
     if (dev < 0 || dev >= 64) return false;
     if (!done[dev]) {
-      if (cudaFuncSetAttribute(fused_u8_tc_kernel<MP, R, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      if (cudaFuncSetAttribute(fused_u8_tc_kernel<MP, R, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)kTcSmem) != cudaSuccess)
         return false;
       done[dev] = true;
     }
   }
   const int64_t grid = (int64_t)a.n_chunks < sms_s() ? (int64_t)a.n_chunks : sms_s();
-  long long* trace = nullptr;
-#ifdef ADCT_TC_TRACE
-  static long long* tbuf = nullptr;
-  if (!tbuf && cudaMalloc(&tbuf, 64 * 16 * sizeof(long long)) != cudaSuccess) tbuf = nullptr;
-  if (tbuf) cudaMemsetAsync(tbuf, 0, 64 * 16 * sizeof(long long), st);
-  trace = tbuf;
-#endif
-  fused_u8_tc_kernel<MP, R, TW><<<(unsigned)grid, kTcThreads, kTcSmem, st>>>(map, a, dm, partial, trace);
-#ifdef ADCT_TC_TRACE
-  if (tbuf) {
-    long long h[64 * 16];
-    cudaMemcpyAsync(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    if (FILE* f = std::fopen("gpurun_out/tc_trace.txt", "w")) {
-      for (int i = 0; i < 64; ++i) {
-        for (int k = 0; k < 16; ++k) std::fprintf(f, "%lld ", h[i * 16 + k] ? h[i * 16 + k] - h[0] : -1);
-        std::fprintf(f, "\n");
-      }
-      std::fclose(f);
-    }
-  }
-#endif
+  fused_u8_tc_kernel<MP, R, CW><<<(unsigned)grid, kTcThreads, kTcSmem, st>>>(map, a, dm, partial);
   return true;
 }
 
 template <class MP, int R>
-bool launch_tc_r(int tw, const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial,
+bool launch_tc_r(int cw, const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial,
                  cudaStream_t st) {
-  if (tw == 128) return launch_tc_rt<MP, R, 128>(map, a, dm, partial, st);
-  return tw == 256 && launch_tc_rt<MP, R, 256>(map, a, dm, partial, st);
+  switch (cw) {
+    case 2: return launch_tc_rc<MP, R, 2>(map, a, dm, partial, st);
+    case 1: return launch_tc_rc<MP, R, 1>(map, a, dm, partial, st);
+    case 16: return launch_tc_rc<MP, R, 16>(map, a, dm, partial, st);
+    default: return false;
+  }
 }
 
 // compiled (matrix, r) pairs: T1 at config 4's r = 10 and the Lena figures' r = 3, 14
 // (P:L2380-2444); runtime integer matrices at r = 10
 template <class MP>
-bool launch_tc(int r, int tw, const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial,
+bool launch_tc(int r, int cw, const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial,
                cudaStream_t st) {
   if constexpr (!MP::kConst) {
-    return r == 10 && launch_tc_r<MP, 10>(tw, map, a, dm, partial, st);
+    return r == 10 && launch_tc_r<MP, 10>(cw, map, a, dm, partial, st);
   } else {
     switch (r) {
-      case 3: return launch_tc_r<MP, 3>(tw, map, a, dm, partial, st);
-      case 10: return launch_tc_r<MP, 10>(tw, map, a, dm, partial, st);
-      case 14: return launch_tc_r<MP, 14>(tw, map, a, dm, partial, st);
+      case 3: return launch_tc_r<MP, 3>(cw, map, a, dm, partial, st);
+      case 10: return launch_tc_r<MP, 10>(cw, map, a, dm, partial, st);
+      case 14: return launch_tc_r<MP, 14>(cw, map, a, dm, partial, st);
       default: return false;
     }
   }
 }
 
+// 5-D map {128 B, 8 rows, bands, chunks, images}, strides {row, 8 rows, 128 B, image}
+bool make_tc_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int cw) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const int64_t istride = g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride;
+  const cuuint64_t dims[5] = {128, 8, (cuuint64_t)(g.height / 8), (cuuint64_t)(g.width / 128),
+                              (cuuint64_t)g.n_images};
+  const cuuint64_t strides[4] = {(cuuint64_t)g.row_stride, (cuuint64_t)(8 * g.row_stride), 128, (cuuint64_t)istride};
+  const cuuint32_t box[5] = {128, 8, (cuuint32_t)(16 / cw), (cuuint32_t)cw, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(src), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
+// tile shape of the tensor-core kernel: CW 128-byte chunks x 16/CW bands, the CW in {2, 16, 1}
+// with the fewest tiles (zero-filled parts of edge tiles cost MMA rows, never HBM bytes)
+TcPlan tc_plan(const adct_geom& g) {
+  TcPlan p{};
+  if (g.width <= 0 || g.height <= 0 || (g.width % 128) != 0) return p;  // whole 128-byte chunks only
+  const int64_t nch = g.width / 128, nbd = g.height / 8;
+  int64_t best = -1;
+  for (int cw : {2, 16, 1}) {
+    const int64_t bh = 16 / cw;
+    const int64_t tiles = ((nch + cw - 1) / cw) * ((nbd + bh - 1) / bh);
+    if (best < 0 || tiles < best) {
+      best = tiles;
+      p.cw = cw;
+    }
+  }
+  p.tpr = (int32_t)((nch + p.cw - 1) / p.cw);
+  p.tpi = (int32_t)(p.tpr * ((nbd + 16 / p.cw - 1) / (16 / p.cw)));
+  p.cpi = (p.tpi + kTcChunkTiles - 1) / kTcChunkTiles;
+  p.n_chunks = g.n_images * (int64_t)p.cpi;
+  p.ok = (g.row_stride % 16) == 0 && (g.n_images <= 1 || (g.image_stride % 16) == 0) &&
+         g.image_stride < ((int64_t)1 << 40) && 8 * g.row_stride < ((int64_t)1 << 40) &&
+         p.n_chunks < ((int64_t)1 << 31);
+  return p;
+}
+
 // The tensor-core streaming path for (u8 source, integer matrix, no clip, one r); false when
-// the geometry or r is not covered (the caller then tries the SIMT streaming kernel).
+// the geometry or r is not covered (the caller then uses the SIMT streaming kernel).
 bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
                  double* partial, cudaStream_t st, adct_status* status) {
-  const WtPlan p = tc_plan(g);
+  const TcPlan p = tc_plan(g);
   if (!p.ok || g.n_images == 0 || !aligned(src, 16) || !m->is_int) return false;
   CUtensorMap map;
-  if (!make_u8_tmap(&map, src, g, p.tw, p.rows)) return false;
+  if (!make_tc_tmap(&map, src, g, p.cw)) return false;
   TcArgs a;
-  a.tpb = p.tpb;
+  a.tpr = p.tpr;
   a.tpi = p.tpi;
   a.cpi = p.cpi;
   a.n_chunks = (uint32_t)p.n_chunks;
   a.dcpi = make_fastdiv((uint32_t)p.cpi);
-  a.dtpb = make_fastdiv((uint32_t)p.tpb);
-  const bool ok = m->specialized ? launch_tc<T1Mat>(r, p.tw, map, a, m->dev, partial, st)
-                                 : launch_tc<RtMat>(r, p.tw, map, a, m->dev, partial, st);
+  a.dtpr = make_fastdiv((uint32_t)p.tpr);
+  const bool ok = m->specialized ? launch_tc<T1Mat>(r, p.cw, map, a, m->dev, partial, st)
+                                 : launch_tc<RtMat>(r, p.cw, map, a, m->dev, partial, st);
   if (!ok) return false;
   count_launch();
   if ((*status = launch_status()) != ADCT_OK) return true;

@@ -13,8 +13,8 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
          ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);
 }
 
-__global__ void contend(long long* out, int mode, int reps, int iw) {
-  __shared__ __align__(1024) uint8_t sB[80 * 64 * 2];
+__global__ void contend(long long* out, int mode, int reps, int iw, int nn, int smsp_mask) {
+  __shared__ __align__(1024) uint8_t sB[160 * 64 * 2];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tbase;
   __shared__ volatile int stop;
@@ -34,7 +34,7 @@ __global__ void contend(long long* out, int mode, int reps, int iw) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm = tbase;
-  constexpr uint32_t idesc = (1u << 4) | (10u << 17) | (8u << 24);  // N = 80, M = 128
+  const uint32_t idesc = (1u << 4) | ((uint32_t)(nn >> 3) << 17) | (8u << 24);  // M = 128
   if (w == iw) {
     if (lane == 0) {
       uint32_t ph = 0;
@@ -70,7 +70,8 @@ __global__ void contend(long long* out, int mode, int reps, int iw) {
     const uint32_t col = 96 + 96 * ((w >> 2) % 4);  // 96..383: not the MMA's columns
     long long n = 0;
     const long long c0 = clock64();
-    while (!stop) {
+    const bool active = (smsp_mask >> (w & 3)) & 1;
+    while (!stop && active) {
       if (mode & 1) {
         uint32_t r[32];
         asm volatile(
@@ -104,6 +105,23 @@ __global__ void contend(long long* out, int mode, int reps, int iw) {
         }
         if (a0 + a1 + a2 + a3 == 1.2345f) out[2] = 1;
       }
+      if (mode & 8) {  // integer ALU work only
+        uint32_t a0 = (uint32_t)n, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+#pragma unroll 16
+        for (int i = 0; i < 256; ++i) {
+          a0 = (a0 ^ 0x9e37u) + a1; a1 = (a1 ^ 0x79b9u) + a2; a2 = (a2 ^ 0x7f4au) + a3; a3 = (a3 ^ 0x7c15u) + a0;
+        }
+        if ((a0 ^ a1 ^ a2 ^ a3) == 0x12345u) out[2] = 1;
+      }
+      if (mode & 16) {  // int -> float conversions only
+        float a0 = 0.f, a1 = 0.f;
+        uint32_t v = (uint32_t)n;
+#pragma unroll 16
+        for (int i = 0; i < 256; ++i) {
+          a0 += __int2float_rn((int)(v + i)); a1 += __int2float_rn((int)(v ^ i));
+        }
+        if (a0 + a1 == 1.2345f) out[2] = 1;
+      }
       ++n;
       if (mode == 0) break;
     }
@@ -117,16 +135,21 @@ __global__ void contend(long long* out, int mode, int reps, int iw) {
 int main() {
   long long* d;
   cudaMalloc(&d, 32);
-  const char* names[8] = {"idle", "ldtm x32", "sttm x16", "ldtm+sttm", "ffma", "ffma+ldtm", "ffma+sttm", "all"};
-  for (int iw = 0; iw < 16; iw += 15)
-  for (int mode = 0; mode < 8; mode += (mode == 0 ? 4 : 3)) {
-    printf("issuer warp %2d  ", iw);
-    contend<<<1, 512>>>(d, mode, 200, iw);
+  const int modes[2] = {0, 4};
+  const char* names[2] = {"idle", "ffma"};
+  const int iw = 15;  // SMSP 3
+  for (int nn : {16, 80, 160})
+  for (int msk : {0xf, 0x7, 0x8})
+  for (int mi = 0; mi < 2; ++mi) {
+    const int mode = modes[mi];
+    if (mode == 0 && msk != 0xf) continue;
+    printf("N=%3d ffma on SMSPs mask %x  ", nn, msk);
+    contend<<<1, 512>>>(d, mode, 200, iw, nn, msk);
     cudaDeviceSynchronize();
     long long h[4];
     cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
     printf("background %-10s: MMA batch (4 x N=80) %lld cycles (issue %lld); background loop %lld cycles/iter (%s)\n",
-           names[mode], h[0], h[3], h[1], cudaGetErrorString(cudaGetLastError()));
+           names[mi], h[0], h[3], h[1], cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
