@@ -494,8 +494,8 @@ def main():
     traffic, ipb = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            nt = json.load(f)
-            traffic, ipb = nt.get("fused_u8_kernel_bytes_per_launch"), nt.get("instructions_per_block")
+            nt = json.load(f)["simt" if os.environ.get("ADCT_HOT") == "simt" else "tc"]
+            traffic, ipb = nt.get("bytes_per_launch"), nt.get("instructions_per_block")
     except Exception:
         pass
 

@@ -10,6 +10,7 @@ invariants and brute force — none of which re-types the oracle's own formula.
   quantiser  exhaustive over Y in [-36720, 36720] against decimal arithmetic
 """
 import decimal
+import fractions
 import itertools
 import math
 
@@ -256,32 +257,62 @@ def test_psnr_closed_forms():
     assert abs(oracle.psnr(npix, npix) - 20 * math.log10(255)) < 1e-12  # MSE = 1 -> 48.13 dB
 
 
+# (position, n_k * n_l) for T1, n = diag(T1 T1^T) = (8, 18, 20, 18, 8, 18, 20, 18): one position per
+# distinct product; 64, 144, 324, 400 have a rational sqrt (ties possible), 160 and 360 do not
+QUANT_POSITIONS = [((0, 0), 64), ((0, 1), 144), ((0, 2), 160), ((1, 1), 324), ((1, 2), 360), ((2, 2), 400)]
+Y_MAX = 36720  # 2 * 18360: covers the int16 sources' range of Y for T1 with margin
+
+
+def _quantize_at(ys, pos):
+    """Oracle quantiser on blocks that hold Y only at `pos` (T1's row norms n)."""
+    n, _ = oracle.row_scaling(M.T1)
+    yb = np.zeros((ys.size, 1, 1, 8, 8), dtype=np.int64)
+    yb[:, 0, 0, pos[0], pos[1]] = ys
+    q = oracle.quantize(yb, n, 16)
+    rest = q.copy()
+    rest[:, 0, 0, pos[0], pos[1]] = 0
+    assert not rest.any()  # zero coefficients quantise to zero
+    return q[:, 0, 0, pos[0], pos[1]].astype(np.int64)
+
+
 def test_quantiser_exhaustive():
-    """|q| = round half away from zero of Y/(16 sqrt(n_k n_l)), decided exactly (reading A10),
-    checked against 40-digit decimal arithmetic for every Y in [-36720, 36720]."""
-    decimal.getcontext().prec = 40
-    ys = np.arange(-36720, 36721, dtype=np.int64)
-    pad = (-ys.size) % 64
-    yb = np.concatenate([ys, np.zeros(pad, dtype=np.int64)]).reshape(-1, 1, 1, 8, 8)
-    nvals = [(8, 8), (8, 18), (8, 20), (18, 18), (18, 20), (20, 20)]
-    for nk, nl in nvals:
-        # n_k on even rows/cols and n_l on odd ones: position (0,1) sees (nk, nl)
-        nmix = np.array([nk, nl, nk, nl, nk, nl, nk, nl], dtype=np.int64)
-        q = oracle.quantize(yb, nmix, 16).reshape(-1)
-        # position (0,1) of every block sees n_k=nk (row 0) and n_l=nl (col 1)
-        qk = q.reshape(-1, 64)[:, 1]
-        yk = yb.reshape(-1, 64)[:, 1]
-        step = decimal.Decimal(16) * decimal.Decimal(nk * nl).sqrt()
-        for yv, qv in zip(yk.tolist(), qk.tolist()):
-            d = decimal.Decimal(yv) / step
-            ref = int(d.copy_abs().quantize(decimal.Decimal(1), rounding=decimal.ROUND_HALF_UP))
-            ref = -ref if yv < 0 else ref
-            assert ref == qv, (nk, nl, yv)
-    # ties exist where sqrt(n_k n_l) is rational: Y = 64 at n = 8x8 is exactly 0.5
-    q = oracle.quantize(np.full((1, 1, 1, 8, 8), 64, dtype=np.int64), np.full(8, 8, dtype=np.int64), 16)
-    assert q[0, 0, 0, 0, 0] == 1
-    q = oracle.quantize(np.full((1, 1, 1, 8, 8), -64, dtype=np.int64), np.full(8, 8, dtype=np.int64), 16)
-    assert q[0, 0, 0, 0, 0] == -1
+    """Reading A10: q = round half away from zero of the real Y / (16 sqrt(n_k n_l)).  For EVERY
+    Y in [-36720, 36720] and each of the six products n_k n_l of T1 (S_1) the oracle
+    equals exact arithmetic done another way: rational products with Fraction (exact, ties
+    included), irrational ones with 50-digit decimals (no ties exist there).  The exact tie counts
+    of SURVEY.md §8(c) A10 follow from the mathematics (|Y| = (2m+1) * 8 sqrt(n_k n_l)) and are
+    asserted, as is the number of ties on which round-half-even (rint) would disagree."""
+    ys = np.arange(-Y_MAX, Y_MAX + 1, dtype=np.int64)
+    decimal.getcontext().prec = 50
+    half = fractions.Fraction(1, 2)
+    expect_ties = {64: (574, 288), 144: (382, 192), 324: (256, 128), 400: (230, 116)}
+    for pos, prod in QUANT_POSITIONS:
+        q = _quantize_at(ys, pos).tolist()
+        root = math.isqrt(prod)
+        ties = rint_disagree = 0
+        if root * root == prod:
+            step = 16 * root
+            for yv, qv in zip(ys.tolist(), q):
+                f = fractions.Fraction(abs(yv), step)
+                fl = f.numerator // f.denominator
+                frac = f - fl
+                ref = fl + 1 if frac >= half else fl
+                if frac == half:
+                    ties += 1
+                    if fl % 2 == 0:  # half-even would keep fl, half-away takes fl + 1
+                        rint_disagree += 1
+                assert qv == (-ref if yv < 0 else ref), (prod, yv)
+            assert (ties, rint_disagree) == expect_ties[prod], prod
+        else:
+            step = decimal.Decimal(16) * decimal.Decimal(prod).sqrt()
+            for yv, qv in zip(ys.tolist(), q):
+                d = decimal.Decimal(abs(yv)) / step
+                fl = int(d)
+                assert abs((d - fl) - decimal.Decimal("0.5")) > decimal.Decimal("1e-30")  # never a tie
+                ref = fl + 1 if d - fl > decimal.Decimal("0.5") else fl
+                assert qv == (-ref if yv < 0 else ref), (prod, yv)
+    # the smallest tie: Y = +-64 at (0, 0) is exactly +-0.5 and rounds away from zero
+    assert _quantize_at(np.array([64, -64, 63, -63, 192, -192]), (0, 0)).tolist() == [1, -1, 0, 0, 2, -2]
 
 
 def test_paper_psnr_ordering_on_ar1_image():
