@@ -2,16 +2,19 @@
 """Benchmark of the hot path of arXiv 1808.02950 on B200 (driver contract).
 
 Workload (BASELINE.json config 4, the configuration the metric "8x8 blocks/s
-(fwd+retain+inv), achieved HBM GB/s vs B200 peak, 1/2/4/8 GPU" is quoted on): per GPU, 512
+(fwd+retain+inv), achieved HBM GB/s vs B200 peak, 1/2/4/8 GPU" is quoted on): ONE stack of 512
 synthetic 3840x2160 8-bit YUV 4:2:0 frames (AR(1) rho = 0.95 luma, rho = 0.9 chroma at half
-resolution), forward approximate DCT with the paper's T1 and S, zonal retention r = 10,
-inverse, per-frame per-plane SSE -> PSNR.  One step = the whole stack (99,532,800 blocks per
-GPU) through the fused C-ABI call for each plane + the NCCL all-reduce of the SSE table.
+resolution), sharded by frame over the GPUs (strong scaling; `--scaling weak` gives every GPU
+its own 512 frames), forward approximate DCT with the paper's T1 and S, zonal retention r = 10,
+inverse, per-frame per-plane SSE and PSNR.  One step = the whole stack (99,532,800 blocks)
+through the fused C-ABI call for each plane of each rank's shard + the NCCL all-reduce of the
+fp64 [512 x 6] SSE/PSNR table (overlapped with the next step's kernels).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--scaling weak]
+    python bench.py --config C5 [--c5-log2 20,22,...,30]      secondary configurations
 
-Prints one JSON line (rank 0).  Inputs (6.37 GB per GPU) are larger than the 126 MB L2, so no
-flush is needed between steps.
+Prints one JSON line (rank 0).  Inputs (6.37 GB per 512 frames; 0.8 GB per GPU at 8 GPUs) are
+larger than the 126 MB L2, so no flush is needed between steps.
 """
 from __future__ import annotations
 
@@ -100,33 +103,54 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_frames(rank: int, device):
-    """This rank's 512 frames (weak scaling: each rank owns its stack; seeds per rank)."""
-    return synth.yuv420_stack(FRAMES, H, W, seed=4 + 1000 * rank, device=device, batch=8)
+def make_frames(lo: int, hi: int, device, seed: int = 4):
+    """Frames [lo, hi) of the 512-frame C4 stack (synth batches are aligned to global frame
+    indices, so a rank's shard equals the same frames of the whole stack)."""
+    return synth.yuv420_stack(FRAMES, H, W, seed=seed, device=device, batch=8, lo=lo, hi=hi)
 
 
-def cpu_oracle_sample(planes_cpu, budget_s: float = 15.0):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_oracle_sample(planes_cpu, budget_s: float = 10.0):
     """The oracle as it stands on a bounded sample of the same workload: whole frames (Y, U, V)
-    taken in order from the first frames of the stack (cycling) until ~budget_s of CPU work."""
+    taken in order from the first frames of the stack (cycling) for ~budget_s of CPU work, once
+    on 1 thread and once on every host thread (SURVEY §8(d) oracle timing)."""
     import oracle
     from oracle import matrices as OM
 
     n_avail = int(planes_cpu[0].shape[0])
-    t0 = time.perf_counter()
-    blocks = frames = 0
-    while True:
-        f = frames % n_avail
-        for p in planes_cpu:
-            oracle.codec_sse(p[f:f + 1].numpy(), [R], t=OM.T1)
-        blocks += BLOCKS_PER_FRAME
-        frames += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": blocks / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{frames} frame(s) (Y+U+V, {blocks} blocks) cycled from the first {n_avail} frames of "
-                      f"the same C4 stack, r={R}, T1, oracle/adct_oracle.c by-definition int64/fp64, OpenMP, "
-                      f"{dt:.1f} s"}
+
+    def rate(threads):
+        oracle.set_num_threads(threads)
+        t0 = time.perf_counter()
+        blocks = frames = 0
+        while True:
+            f = frames % n_avail
+            for p in planes_cpu:
+                oracle.codec_sse(p[f:f + 1].numpy(), [R], t=OM.T1)
+            blocks += BLOCKS_PER_FRAME
+            frames += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        return blocks / (time.perf_counter() - t0), frames, blocks
+
+    nproc = os.cpu_count() or 1
+    v1, f1, b1 = rate(1)
+    vn, fn, bn = rate(nproc)
+    return {"value": vn, "unit": UNIT, "cores": nproc, "kind": "oracle", "value_1thread": v1,
+            "nproc": nproc, "cpu_model": cpu_model(),
+            "sample": f"whole C4 frames (Y+U+V, 194,400 blocks each) cycled from the first {n_avail} frames of the "
+                      f"same stack, r={R}, T1, oracle/adct_oracle.c by-definition int64/fp64: {fn} frames on {nproc} "
+                      f"OpenMP threads and {f1} on 1 thread, ~{budget_s:.0f} s each"}
 
 
 def run_reference(args):
@@ -153,7 +177,8 @@ def run_reference(args):
     value = BLOCKS_PER_FRAME * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": getattr(args, "scaling", "strong"),
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample_per_step": "1 frame (Y+U+V, 194,400 blocks)", "matrix": "T1",
                    "r": R},
@@ -203,16 +228,20 @@ def run_config(args):
     driver's headline line is config 4).  One JSON line per (config, matrix)."""
     import oracle
     from oracle import matrices as OM
-    from paper_1808_02950_b200 import adct, catalog
+    from paper_1808_02950_b200 import adct, catalog, parallel
 
-    dev = torch.device("cuda", 0)
+    rank, local, world = parallel.init()
+    if world > 1 and args.config != "C5":
+        raise SystemExit("only --config C5 shards over GPUs (the other secondary configs are 1-GPU lines)")
+    dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
     hbm_peak, peak_kind = peaks()
     lines = []
 
     def emit(cfg, matrix, ms, blocks, bytes_per_block, bound, clk, cpu, extra=None, roofline=None):
-        achieved = blocks * bytes_per_block / (ms * 1e-3) / 1e9
+        # per-GPU HBM roofline: the GPUs of a sharded line each move blocks / n_gpus
+        achieved = blocks * bytes_per_block / (ms * 1e-3) / 1e9 / ((extra or {}).get("n_gpus") or 1)
         line = {"metric": METRIC, "value": blocks / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f32",
                 "data": "synthetic", "config": {"workload": cfg, "matrix": matrix},
@@ -247,29 +276,51 @@ def run_config(args):
              "quantiser -> int16 block-major", "T1", ms, blocks, 192, "hbm", clk, cpu)
         del imgs, q
     if args.config in ("C5", "all"):
-        nblk = 1 << args.c5_log2
-        x = synth.laplace_blocks(nblk, seed=5, device=dev).reshape(nblk, 8, 8)
-        rec = torch.empty_like(x)
-        for name in ("T1", "DCT"):
-            m = adct.Matrix.from_int(catalog.T1, "T1") if name == "T1" else adct.Matrix.from_real(
-                catalog.exact_dct(), "DCT")
-            ms, clk = _timed(lambda: adct.approx_dct8x8_roundtrip(m, x, 64, torch.int16, recon=rec, stream=stream),
-                             args.steps, args.warmup, stream, dev)
-            ok = bool(torch.equal(rec, x))
-            xs = x[:1 << 14].cpu().numpy()
-            if name == "T1":
-                n_, s_ = oracle.row_scaling(OM.T1)
-                g_, _ = oracle.synthesis_matrix(oracle.chat_from_int(OM.T1))
-                fn = lambda: oracle.inverse(g_, oracle.scale(oracle.forward_int(OM.T1, xs), s_))  # noqa: E731
-            else:
-                g_, _ = oracle.synthesis_matrix(OM.C)
-                fn = lambda: oracle.inverse(g_, oracle.forward_real(OM.C, xs))  # noqa: E731
-            cpu = cpu_rate(fn, 1 << 14)
-            cpu["sample"] = "2^14 blocks, by-definition forward + inverse"
-            emit(f"C5: 2^{args.c5_log2} int16 Laplace(10) blocks, fused forward + inverse (r=64) -> int16, "
-                 f"in-place-sized out-of-place", name, ms, nblk, 256, "hbm", clk, cpu,
-                 {"roundtrip_bit_exact": ok})
-        del x, rec
+        # BASELINE C5: 2^20 .. 2^30 int16 residual blocks, fused forward + inverse (r = 64) with T1
+        # and with the exact DCT through the same path; blocks sharded by contiguous range over the
+        # ranks with no collective; 2^30 blocks (137 GB) run IN PLACE (recon is src)
+        for lg in [int(v) for v in str(args.c5_log2).split(",")]:
+            nblk = 1 << lg
+            lo, hi = parallel.shard_range(nblk, rank, world)
+            in_place = lg >= 29
+            x = synth.laplace_range(lo, hi, seed=5, device=dev)
+            rec = x if in_place else torch.empty_like(x)
+            steps = max(5, min(args.steps, args.steps * (1 << 26) // nblk))
+            for name in ("T1", "DCT"):
+                m = adct.Matrix.from_int(catalog.T1, "T1") if name == "T1" else adct.Matrix.from_real(
+                    catalog.exact_dct(), "DCT")
+                parallel.barrier()
+                ms, clk = _timed(lambda: adct.approx_dct8x8_roundtrip(m, x, 64, torch.int16, recon=rec,
+                                                                      stream=stream), steps, args.warmup, stream, dev)
+                ms = parallel.max_over_ranks(ms, dev)
+                # r = 64 round trip is the identity after rounding (bit-exact): in place, x must
+                # still equal the generated blocks after every step; checked on sampled batches
+                if in_place:
+                    smp = sorted({0, (hi - lo) // 2, max(0, hi - lo - 4096)})
+                    ok = all(torch.equal(x[a0:a0 + 4096],
+                                         synth.laplace_range(lo + a0, min(hi, lo + a0 + 4096), seed=5, device=dev))
+                             for a0 in smp)
+                else:
+                    ok = bool(torch.equal(rec, x))
+                if rank != 0:
+                    continue
+                xs = x[:1 << 14].cpu().numpy()
+                if name == "T1":
+                    n_, s_ = oracle.row_scaling(OM.T1)
+                    g_, _ = oracle.synthesis_matrix(oracle.chat_from_int(OM.T1))
+                    fn = lambda: oracle.inverse(g_, oracle.scale(oracle.forward_int(OM.T1, xs), s_))  # noqa: E731
+                else:
+                    g_, _ = oracle.synthesis_matrix(OM.C)
+                    fn = lambda: oracle.inverse(g_, oracle.forward_real(OM.C, xs))  # noqa: E731
+                cpu = cpu_rate(fn, 1 << 14)
+                cpu["sample"] = "2^14 blocks, by-definition forward + inverse"
+                emit(f"C5: 2^{lg} int16 Laplace(10) blocks, fused forward + inverse (r=64) -> int16, "
+                     f"{'in place' if in_place else 'out of place'}, blocks sharded over {world} GPU(s)", name, ms,
+                     nblk, 256, "hbm", clk, cpu,
+                     {"roundtrip_bit_exact": ok, "n_gpus": world, "scaling": "strong", "log2_blocks": lg,
+                      "in_place": in_place, "steps": steps})
+            del x, rec
+            torch.cuda.empty_cache()
     if args.config in ("MERIT", "all"):
         # next row f4: Table 4 figures of merit of the nine matrices over 4096 values of rho in
         # (0, 1) — the Fig. 1 coding-gain curves
@@ -406,6 +457,8 @@ def run_config(args):
             emit("C2: 45 AR(1) 512x512 images, r = 1..64 curves for the 9 matrices (T1, C, T2, LO, SDCT, RDCT, "
                  "BAS-2008b, T4, T6) through the same kernel; value counts block x matrix", "all 9", ms,
                  45 * 4096 * 9, 64, "alu", clk, cpu, roofline=issue_roofline("C2", ms, clk, dev))
+    if world > 1:
+        torch.distributed.destroy_process_group()
     return 0
 
 
@@ -418,9 +471,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default, BASELINE C4): one 512-frame stack sharded over the GPUs; "
+                         "weak: 512 frames per GPU")
     ap.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C5", "SSIM", "JAM", "GREEDY", "MERIT", "all"],
                     help="secondary BASELINE.json configuration instead of the config-4 headline")
-    ap.add_argument("--c5-log2", type=int, default=26)
+    ap.add_argument("--c5-log2", default="20,22,24,26,28,30",
+                    help="comma-separated log2 block counts of the C5 sweep (>= 29 runs in place)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -434,34 +491,47 @@ def main():
     rank, local, world = parallel.init()
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(dev)  # the error-table all-reduce overlaps the next step's kernels
     m = adct.Matrix.from_int(catalog.T1, "T1")
-    planes = make_frames(rank, dev)  # Y [512,2160,3840], U/V [512,1080,1920]
+    if args.scaling == "strong":
+        # BASELINE C4: ONE 512-frame stack sharded over the ranks, [floor(qN/W), floor((q+1)N/W))
+        n_total = FRAMES
+        lo, hi = parallel.shard_range(FRAMES, rank, world)
+        planes = make_frames(lo, hi, dev)
+    else:
+        # weak scaling (--scaling weak): every rank owns its own 512-frame stack
+        n_total = world * FRAMES
+        lo, hi = rank * FRAMES, (rank + 1) * FRAMES
+        planes = make_frames(0, FRAMES, dev, seed=4 + 1000 * rank)
+    n_local = hi - lo
     torch.cuda.synchronize(dev)
     geoms = [adct.geom_of(p) for p in planes]
     ws = torch.empty(max(adct.workspace_bytes(g, 1) for g in geoms), dtype=torch.uint8, device=dev)
-    # global per-frame, per-plane table (fp64): `local` holds this rank's rows (the others stay
-    # zero; the kernels write their per-frame SSE straight into it); every step it is copied into
-    # `table` and all-reduced, so each entry has exactly one non-zero contributor and the result
-    # is bit-identical to a single GPU
-    etab = parallel.ErrorTable(world * FRAMES, 3, rank * FRAMES, (rank + 1) * FRAMES, device=dev)
-    table = etab.table
-    lo = rank * FRAMES
+    # the global per-frame table (fp64, columns SSE Y/U/V, PSNR Y/U/V): the kernels write this
+    # rank's rows directly; each step's buffer is all-reduced on the side stream while the next
+    # step runs (every entry has exactly one non-zero contributor: bit-identical to one GPU)
+    etab = parallel.ErrorTable(n_total, 6, lo, hi, device=dev, buffers=2)
 
     # per-step events around the luma launch (the dominant kernel), on the launching stream
     ev_luma = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
 
-    def step(k=None):
+    def step(k, timed=False):
+        buf = k % 2
+        etab.before_write(buf)
         for i, p in enumerate(planes):
-            if k is not None and i == 0:
+            if timed and i == 0:
                 ev_luma[k][0].record(stream)
-            adct.approx_dct8x8_fused_sse(m, p, [R], workspace=ws, sse=etab.out(i), stream=stream)
-            if k is not None and i == 0:
+            adct.approx_dct8x8_fused_sse(m, p, [R], workspace=ws, sse=etab.out(i, buf), psnr=etab.out(3 + i, buf),
+                                         stream=stream)
+            if timed and i == 0:
                 ev_luma[k][1].record(stream)
-        etab.combine()
+        etab.combine(buf, stream=side)
+        return buf
 
-    for _ in range(args.warmup):
-        step()
+    for k in range(args.warmup):
+        last = step(k)
+    etab.wait(last)
     torch.cuda.synchronize(dev)
     parallel.barrier()
     torch.cuda.synchronize(dev)
@@ -473,7 +543,8 @@ def main():
             torch.cuda.profiler.start()
         e0.record(stream)
         for k in range(args.steps):
-            step(k)
+            last = step(k, timed=True)
+        etab.wait(last)  # the last step's all-reduce is inside the timed region
         e1.record(stream)
         torch.cuda.synchronize(dev)
         if profile_range:
@@ -482,13 +553,15 @@ def main():
     parallel.barrier()
     total_ms = e0.elapsed_time(e1)
     ms_step = parallel.max_over_ranks(total_ms / args.steps, dev)
-    blocks_step_rank = FRAMES * BLOCKS_PER_FRAME
-    value = world * blocks_step_rank / (ms_step * 1e-3)
+    blocks_total = n_total * BLOCKS_PER_FRAME
+    value = blocks_total / (ms_step * 1e-3)
+    table = etab.table_of(last)
 
-    # dominant kernel: the luma fused launch (fused_u8_wtile_kernel + its finalize_kernel;
-    # 66,355,200 blocks x 64 algorithmic bytes), averaged over the timed steps
+    # dominant kernel: this rank's luma launch (fused_u8_tc_kernel + its finalize_kernel;
+    # n_local x 32,400 blocks x 64 algorithmic bytes), averaged over the timed steps
     luma_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_luma)
-    luma_bytes = FRAMES * (H // 8) * (W // 8) * 64
+    luma_blocks = n_local * (H // 8) * (W // 8)
+    luma_bytes = luma_blocks * 64
     hbm_peak, peak_kind = peaks()
     achieved = luma_bytes / (luma_ms * 1e-3) / 1e9
     traffic, ipb = None, None
@@ -496,13 +569,13 @@ def main():
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             nt = json.load(f)["simt" if os.environ.get("ADCT_HOT") == "simt" else "tc"]
             traffic, ipb = nt.get("bytes_per_launch"), nt.get("instructions_per_block")
+            if traffic is not None:  # recorded for the 512-frame luma launch; per launch here
+                traffic = traffic * n_local / FRAMES
     except Exception:
         pass
 
-    # sanity: PSNR of frame 0 planes (host-side report only)
-    sse0 = table[lo].cpu()
-    npix = [H * W, H * W // 4, H * W // 4]
-    psnr0 = [10 * np.log10(255.0 ** 2 / (float(sse0[i]) / npix[i])) for i in range(3)]
+    # per-plane PSNR of the first frame of the stack, from the library (finalize kernel, fp64)
+    row0 = table[0].cpu()
 
     # end-to-end through the host-buffer C-ABI call (pinned host frames, H2D + D2H inside)
     e2e = None
@@ -511,20 +584,28 @@ def main():
         chunk = 16
         hws = torch.empty(max(adct.host_workspace_bytes(adct.geom_of(h), 1, chunk) for h in host),
                           dtype=torch.uint8, device=dev)
-        out = [torch.empty((FRAMES, 1), dtype=torch.float64).pin_memory() for _ in range(3)]
-        for i, h in enumerate(host):  # warm-up
-            adct.approx_dct8x8_fused_sse_host(m, h, [R], hws, chunk, sse_host=out[i], stream=stream)
+        out = [torch.empty((n_local, 1), dtype=torch.float64).pin_memory() for _ in range(3)]
+        pout = [torch.empty((n_local, 1), dtype=torch.float64).pin_memory() for _ in range(3)]
+
+        def e2e_step():
+            for i, h in enumerate(host):
+                adct.approx_dct8x8_fused_sse_host(m, h, [R], hws, chunk, sse_host=out[i], psnr_host=pout[i],
+                                                  stream=stream)
+
+        e2e_step()  # warm-up
         parallel.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            for i, h in enumerate(host):
-                adct.approx_dct8x8_fused_sse_host(m, h, [R], hws, chunk, sse_host=out[i], stream=stream)
+            e2e_step()
         dt = parallel.max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, dev)
-        assert torch.equal(out[0][:, 0], table[lo:lo + FRAMES, 0].cpu())
-        e2e = {"value": world * blocks_step_rank / dt, "unit": UNIT,
+        for i in range(3):
+            assert torch.equal(out[i][:, 0], table[lo:hi, i].cpu()) and torch.equal(pout[i][:, 0],
+                                                                                    table[lo:hi, 3 + i].cpu())
+        e2e = {"value": blocks_total / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(sum(h.numel() for h in host)),
-               "d2h_bytes_per_step": int(3 * FRAMES * 8), "ms_per_step": dt * 1e3,
-               "path": "approx_dct8x8_fused_sse_host (pinned host frames, 2-stream H2D/compute overlap)"}
+               "d2h_bytes_per_step": int(6 * n_local * 8), "ms_per_step": dt * 1e3,
+               "path": "approx_dct8x8_fused_sse_host (pinned host frames, 2-stream H2D/compute overlap; "
+                       "SSE + PSNR tables back to the host)"}
         del host
 
     cpu = None
@@ -532,33 +613,40 @@ def main():
         cpu = cpu_oracle_sample([p[:16].cpu() for p in planes])
 
     if rank == 0:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        clk_mhz = clk.summary()["sm_mhz"] or 1965
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "frames_per_gpu": FRAMES, "blocks_per_step_per_gpu": blocks_step_rank,
-                       "matrix": "T1", "r": R, "parallelism": f"dp{world} (frames sharded, SSE all-reduce)",
-                       "l2": "inputs 6.37 GB/GPU > 126 MB L2, no flush",
-                       "hbm_gbs_step": world * blocks_step_rank * 64 / (ms_step * 1e-3) / 1e9 / world},
+            "config": {"workload": WORKLOAD, "frames_total": n_total, "frames_per_gpu": n_local,
+                       "blocks_per_step": blocks_total, "matrix": "T1", "r": R,
+                       "parallelism": f"dp{world} ({'one 512-frame stack' if args.scaling == 'strong' else '512 frames per GPU'}"
+                                      f" sharded by frame, fp64 SSE/PSNR table all-reduce overlapped)",
+                       "l2": "inputs 6.37 GB per 512 frames > 126 MB L2, no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": ("fused_u8_wtile_kernel<T1Mat,10> (SIMT)" if os.environ.get("ADCT_HOT") == "simt" else "fused_u8_tc_kernel<T1Mat,10> (tcgen05 kind::i8)") + " + finalize_kernel (luma plane, 66,355,200 blocks x 64 B)",
+                         "kernel": ("fused_u8_wtile_kernel<T1Mat,10> (SIMT)" if os.environ.get("ADCT_HOT") == "simt"
+                                    else "fused_u8_tc_kernel<T1Mat,10> (tcgen05 kind::i8)") +
+                                   f" + finalize_kernel (luma plane, {luma_blocks:,} blocks x 64 B)",
                          "kernel_ms": luma_ms},
+            # the whole step (Y + U + V + finalizes + the table combine), rank 0's share
+            "roofline_step": {"bound": "hbm", "achieved": n_local * BLOCKS_PER_FRAME * 64 / (ms_step * 1e-3) / 1e9,
+                              "peak": hbm_peak, "unit": "GB/s",
+                              "frac": n_local * BLOCKS_PER_FRAME * 64 / (ms_step * 1e-3) / 1e9 / hbm_peak},
             "clocks": clk.summary(),
-            # the binding constraint of the hot kernel: one warp-instruction per
-            # clock per SMSP; roof = SMs x 4 x clock x 32 lanes / (SASS instructions per block)
+            # issue view of the hot kernel: one warp-instruction per clock per
+            # SMSP; roof = SMs x 4 x clock x 32 lanes / (thread-instructions per block, ncu)
             "issue_roofline": None if not ipb else {
                 "instructions_per_block": ipb,
-                "roof_blocks_per_s": torch.cuda.get_device_properties(dev).multi_processor_count * 4 *
-                                     (clk.summary()["sm_mhz"] or 1965) * 1e6 * 32 / ipb,
-                "achieved_blocks_per_s": FRAMES * (H // 8) * (W // 8) / (luma_ms * 1e-3),
-                "frac": FRAMES * (H // 8) * (W // 8) / (luma_ms * 1e-3) /
-                        (torch.cuda.get_device_properties(dev).multi_processor_count * 4 *
-                         (clk.summary()["sm_mhz"] or 1965) * 1e6 * 32 / ipb)},
+                "roof_blocks_per_s": sms * 4 * clk_mhz * 1e6 * 32 / ipb,
+                "achieved_blocks_per_s": luma_blocks / (luma_ms * 1e-3),
+                "frac": luma_blocks / (luma_ms * 1e-3) / (sms * 4 * clk_mhz * 1e6 * 32 / ipb)},
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "psnr_frame0_dB": {"Y": psnr0[0], "U": psnr0[1], "V": psnr0[2]},
+            "sse_frame0": {"Y": float(row0[0]), "U": float(row0[1]), "V": float(row0[2])},
+            "psnr_frame0_dB": {"Y": float(row0[3]), "U": float(row0[4]), "V": float(row0[5])},
         }
         print(json.dumps(line), flush=True)
     if parallel.env_rank()[2] > 1:

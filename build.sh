@@ -7,12 +7,19 @@ OUT=$PKG/libadct.so
 mkdir -p build
 FLAGS="-std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -Iinclude -I$PKG/csrc --expt-relaxed-constexpr -Xptxas -v"
 pids=()
+# incremental: an object is rebuilt when its .cu, any shared header or this script is newer
+# (FORCE=1 rebuilds everything)
+HDRS="$PKG/csrc/*.cuh $PKG/csrc/*.h include/*.h build.sh"
 for f in matrix basic fused stream tc sweep blockmajor jam greedy merit; do
-  nvcc $FLAGS -c $PKG/csrc/$f.cu -o build/$f.o > build/$f.ptxas.log 2>&1 &
+  o=build/$f.o
+  if [ "${FORCE:-0}" != 1 ] && [ -f $o ] && [ -z "$(find $PKG/csrc/$f.cu $HDRS -newer $o 2>/dev/null)" ]; then
+    continue
+  fi
+  nvcc $FLAGS -c $PKG/csrc/$f.cu -o $o.tmp > build/$f.ptxas.log 2>&1 && mv $o.tmp $o &
   pids+=($!)
 done
 rc=0
-for p in "${pids[@]}"; do wait $p || rc=1; done
+for p in "${pids[@]:-}"; do [ -n "$p" ] && { wait $p || rc=1; }; done
 if [ $rc -ne 0 ]; then cat build/*.ptxas.log | grep -v "^ptxas info" | head -50; exit 1; fi
 nvcc -shared -gencode arch=compute_100a,code=sm_100a -o $OUT.tmp build/matrix.o build/basic.o build/fused.o build/stream.o build/tc.o build/sweep.o build/blockmajor.o build/jam.o build/greedy.o build/merit.o
 mv $OUT.tmp $OUT

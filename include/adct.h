@@ -164,11 +164,18 @@ adct_status approx_dct_jam_roundtrip(int32_t n, const void* src, adct_dtype src_
  * out: DEVICE int32 [n_orders][64] (zero for infeasible sequences); status: DEVICE int32
  * [n_orders], 0 = ok, 1 = no orthogonal candidate left at some step (A24), 2 = invalid
  * sequence (an index outside 0..7, a fixed row, or a repeated row).
+ * ties: DEVICE int32 [n_orders][4] or NULL -- the exact ties met (several orthogonal candidates
+ * with the same fp64 score; the earliest was taken, A22; the paper's §3.4 examples have such
+ * ties): {steps with a tie, row of the first tie (-1 if none), number of tied
+ * candidates at the first tie, largest number of tied candidates at any step}; the steps counted
+ * are those actually searched (up to an infeasible step, none for an invalid sequence).
+ * The search space may be any entry set P, e.g. the extended sets of P:L1206-1235
+ * ({0,+-1,+-4}, {0,+-1,+-8}, {0,+-1,+-2,+-4}, ...; |D| = |P|^8).
  * workspace >= adct_greedy_workspace_bytes(n_entries) (the packed space and the scores). */
 size_t adct_greedy_workspace_bytes(int32_t n_entries);
 adct_status adct_greedy_search(const double c[64], const int32_t* entries, int32_t n_entries, const int32_t fixed[64],
                                uint32_t fixed_mask, const int32_t* orders, int32_t n_orders, int32_t* out,
-                               int32_t* status, void* workspace, size_t workspace_bytes, void* stream);
+                               int32_t* status, int32_t* ties, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Matrix figures of merit of §4.2 for every (matrix, rho) pair: Table 4's
  * total error energy eps = pi ||C - C_hat||_F^2, MSE = tr((C - C_hat) R_x (C - C_hat)^T)/8,
@@ -202,27 +209,35 @@ adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
  * I16 samples with geometry g (8-byte / 16-byte aligned rows); recon: device, same geometry,
  * dtype recon_t with the clip policy of approx_dct8x8_inv, except that the clip range is the
  * source's sample range ([0,255] for U8, [-32768,32767] for I16).  r in 1..64 else
- * ADCT_E_INVALID_ARGUMENT.  Any matrix (integer or real). */
+ * ADCT_E_INVALID_ARGUMENT.  Any matrix (integer or real).  In place is allowed: recon may be
+ * src itself (same pointer, geometry and dtype; BASELINE config 5 runs 2^30 blocks = 137 GB in
+ * place) -- every block is read completely before its reconstruction is written, by the thread
+ * or warp that owns it; any other overlap of src and recon is undefined. */
 adct_status approx_dct8x8_roundtrip(const adct_matrix* m, const void* src, adct_dtype src_t, adct_geom g, int32_t r,
                                     void* recon, adct_dtype recon_t, adct_clip clip, void* stream);
 
-/* Forward -> retain r -> inverse -> clip -> per-image SSE for every r in r_list, reading
- * each block once.  r_list: HOST array of n_r values in 1..64 (n_r <= 64).
- * sse: device fp64 [n_images][n_r].  workspace >= adct_workspace_bytes(g, n_r). */
+/* Forward -> retain r -> inverse -> clip -> per-image SSE and PSNR for every r in r_list,
+ * reading each block once (PSNR per image and per plane, P:L2258-2265, P:L2868;
+ * reading A7).  r_list: HOST array of n_r values in 1..64 (n_r <= 64).
+ * sse: device fp64 [n_images][n_r] (required).  psnr: device fp64 [n_images][n_r] or NULL:
+ * psnr = 10 log10(255^2 / (sse / (H W))), +inf where sse == 0 (r = 64), computed in fp64 by the
+ * library's finalize kernel from the same sum.  workspace >= adct_workspace_bytes(g, n_r). */
 adct_status approx_dct8x8_fused_sse(const adct_matrix* m, const void* src, adct_dtype src_t, adct_geom g,
-                                    const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse,
+                                    const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse, double* psnr,
                                     void* workspace, size_t workspace_bytes, void* stream);
 
-/* The same on HOST buffers: src is a host (preferably pinned) image stack with geometry
- * g, sse a host fp64 [n_images][n_r].  The library stages chunks of images through the
- * caller's device workspace (>= adct_host_workspace_bytes(g, n_r, chunk_images)),
- * overlapping host->device copies with compute on two streams, and synchronises before
- * returning.  chunk_images = images per chunk (>= 1). */
+/* The same on HOST buffers: src is a host (preferably pinned) dense image stack with geometry
+ * g (image_stride == H*row_stride when n_images > 1, else ADCT_E_INVALID_ARGUMENT; a lone
+ * image's image_stride is ignored), sse_host a host fp64 [n_images][n_r], psnr_host the same
+ * or NULL.  The library stages chunks of images through the caller's device workspace
+ * (>= adct_host_workspace_bytes(g, n_r, chunk_images, src_t)), overlapping host->device copies
+ * with compute on two streams, and synchronises before returning.  chunk_images = images per
+ * chunk (>= 1). */
 size_t adct_host_workspace_bytes(adct_geom g, int32_t n_r, int64_t chunk_images, adct_dtype src_t);
 adct_status approx_dct8x8_fused_sse_host(const adct_matrix* m, const void* src_host, adct_dtype src_t, adct_geom g,
                                          const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse_host,
-                                         int64_t chunk_images, void* workspace, size_t workspace_bytes,
-                                         void* stream);
+                                         double* psnr_host, int64_t chunk_images, void* workspace,
+                                         size_t workspace_bytes, void* stream);
 
 /* Forward transform with S folded into a uniform quantiser (BASELINE.json config 3):
  * q_kl = round_half_away(Y_kl / (step * sqrt(n_k n_l)))  (reading A10), int16 block-major.

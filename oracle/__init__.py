@@ -49,6 +49,8 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(_LIB)
         P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
         L.oracle_num_threads.restype = ctypes.c_int
+        L.oracle_set_num_threads.argtypes = [ctypes.c_int]
+        L.oracle_set_num_threads.restype = None
         L.oracle_zigzag_order.argtypes = [P]
         L.oracle_row_scaling.argtypes = [P, P, P]
         L.oracle_chat_from_int.argtypes = [P, P]
@@ -91,6 +93,11 @@ def _img3(img: np.ndarray) -> np.ndarray:
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of later oracle calls (timing only; results are thread-count independent)."""
+    lib().oracle_set_num_threads(int(n))
 
 
 def zigzag_order() -> np.ndarray:

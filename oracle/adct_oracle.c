@@ -44,6 +44,16 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* Timing only (bench.py cpu_baseline): the OpenMP thread count of later calls.  The results do
+ * not depend on it (per-block work, per-image sums in block order). */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : 1);
+#else
+  (void)n;
+#endif
+}
+
 /* ---- zig-zag order (reading A5: JPEG order) ---------------------------
  * Built from the anti-diagonal rule: coefficients are visited by increasing k+l; on an
  * odd anti-diagonal k increases, on an even one k decreases.  order[z] = k*8+l. */

@@ -61,10 +61,10 @@ def _load() -> ctypes.CDLL:
     L.zonal_retain.argtypes = [P, S, I64_, I32_, P]
     L.approx_dct8x8_inv.argtypes = [P, P, S, Geom, P, S, S, P]
     L.psnr_reduce.argtypes = [P, S, P, S, Geom, D, S, P, P, P, ctypes.c_size_t, P]
-    L.approx_dct8x8_fused_sse.argtypes = [P, P, S, Geom, P, I32_, S, P, P, ctypes.c_size_t, P]
+    L.approx_dct8x8_fused_sse.argtypes = [P, P, S, Geom, P, I32_, S, P, P, P, ctypes.c_size_t, P]
     L.adct_host_workspace_bytes.argtypes = [Geom, I32_, I64_, S]
     L.adct_host_workspace_bytes.restype = ctypes.c_size_t
-    L.approx_dct8x8_fused_sse_host.argtypes = [P, P, S, Geom, P, I32_, S, P, I64_, P, ctypes.c_size_t, P]
+    L.approx_dct8x8_fused_sse_host.argtypes = [P, P, S, Geom, P, I32_, S, P, P, I64_, P, ctypes.c_size_t, P]
     L.approx_dct8x8_fwd_quant.argtypes = [P, P, Geom, I32_, P, P]
     L.approx_dct8x8_roundtrip.argtypes = [P, P, S, Geom, I32_, P, S, S, P]
     L.ssim_reduce.argtypes = [P, S, P, S, Geom, D, S, P, P, ctypes.c_size_t, P]
@@ -73,7 +73,7 @@ def _load() -> ctypes.CDLL:
     L.adct_greedy_workspace_bytes.restype = ctypes.c_size_t
     L.adct_merit_batch.argtypes = [P, P, P, I32_, P, I32_, P, P]
     L.adct_matrix_chat.argtypes = [P, P]
-    L.adct_greedy_search.argtypes = [P, P, I32_, P, ctypes.c_uint32, P, I32_, P, P, P, ctypes.c_size_t, P]
+    L.adct_greedy_search.argtypes = [P, P, I32_, P, ctypes.c_uint32, P, I32_, P, P, P, P, ctypes.c_size_t, P]
     L.adct_workspace_bytes.argtypes = [Geom, I32_]
     L.adct_workspace_bytes.restype = ctypes.c_size_t
     L.adct_status_str.argtypes = [S]
@@ -292,9 +292,12 @@ def approx_dct_jam_roundtrip(n: int, src: torch.Tensor, r: int, recon_dtype=torc
     return recon
 
 
-def greedy_search(c, entries, orders, fixed: dict | None = None, device=None, workspace=None, stream=None):
+def greedy_search(c, entries, orders, fixed: dict | None = None, device=None, workspace=None, stream=None,
+                  return_ties: bool = False):
     """Greedy angle search (§3, Fig. 2) for every sequence in `orders` ([n, n_free] row indices):
-    returns (matrices int32 [n, 8, 8], status int32 [n]) on `device`."""
+    returns (matrices int32 [n, 8, 8], status int32 [n]) on `device`, plus with return_ties=True
+    the exact ties met, int32 [n, 4] = (steps with a tie, first tied row or -1, candidates tied
+    there, largest tie) -- see adct_greedy_search in include/adct.h."""
     import numpy as _np
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     c64 = _np.ascontiguousarray(_np.asarray(c, dtype=_np.float64).reshape(64))
@@ -308,13 +311,14 @@ def greedy_search(c, entries, orders, fixed: dict | None = None, device=None, wo
     n = od.shape[0]
     out = torch.empty((n, 8, 8), dtype=torch.int32, device=dev)
     status = torch.empty(n, dtype=torch.int32, device=dev)
+    ties = torch.empty((n, 4), dtype=torch.int32, device=dev) if return_ties else None
     nbytes = lib.adct_greedy_workspace_bytes(len(ent))
     if workspace is None or workspace.numel() < nbytes:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     _check(lib.adct_greedy_search(c64.ctypes.data, ent.ctypes.data, len(ent), fx.ctypes.data, mask, od.data_ptr(), n,
-                                  out.data_ptr(), status.data_ptr(), workspace.data_ptr(), workspace.numel(),
-                                  _stream_ptr(stream)), "adct_greedy_search")
-    return out, status
+                                  out.data_ptr(), status.data_ptr(), _ptr(ties), workspace.data_ptr(),
+                                  workspace.numel(), _stream_ptr(stream)), "adct_greedy_search")
+    return (out, status, ties) if return_ties else (out, status)
 
 
 def merit_batch(mats: list, rho: torch.Tensor, c_exact=None, stream=None) -> torch.Tensor:
@@ -375,22 +379,29 @@ def approx_dct8x8_roundtrip(m: Matrix, src: torch.Tensor, r: int = 64, recon_dty
 
 def approx_dct8x8_fused_sse(m: Matrix, src: torch.Tensor, r_list, clip: int = CLIP_NONE,
                             workspace: torch.Tensor | None = None, sse: torch.Tensor | None = None,
-                            stream=None) -> torch.Tensor:
-    """SSE [n, len(r_list)] (fp64, device) of forward -> retain r -> inverse per image."""
+                            stream=None, psnr: torch.Tensor | None = None, return_psnr: bool = False):
+    """SSE [n, len(r_list)] (fp64, device) of forward -> retain r -> inverse per image; with
+    `psnr` (an output tensor) or return_psnr=True also the library's PSNR: returns (sse, psnr)."""
     g = geom_of(src)
     rl = [int(r) for r in r_list]
     arr = (ctypes.c_int32 * len(rl))(*rl)
     if sse is None:
         sse = torch.empty((g.n_images, len(rl)), dtype=torch.float64, device=src.device)
     _out(sse, g.n_images * len(rl), src, "sse", dtype=torch.float64)
+    want_psnr = return_psnr or psnr is not None
+    if want_psnr and psnr is None:
+        psnr = torch.empty((g.n_images, len(rl)), dtype=torch.float64, device=src.device)
+    if want_psnr:
+        _out(psnr, g.n_images * len(rl), src, "psnr", dtype=torch.float64)
     nbytes = workspace_bytes(g, len(rl))
     if workspace is None or workspace.numel() < nbytes:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=src.device)
     _check(lib.approx_dct8x8_fused_sse(m.handle, src.data_ptr(), dtype_code(src), g,
                                        ctypes.cast(arr, ctypes.c_void_p), len(rl), int(clip), sse.data_ptr(),
-                                       workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)),
+                                       psnr.data_ptr() if want_psnr else None, workspace.data_ptr(),
+                                       workspace.numel(), _stream_ptr(stream)),
            "approx_dct8x8_fused_sse")
-    return sse
+    return (sse, psnr) if want_psnr else sse
 
 
 def host_workspace_bytes(geom: Geom, n_r: int, chunk_images: int, src_dtype: int = U8) -> int:
@@ -399,19 +410,26 @@ def host_workspace_bytes(geom: Geom, n_r: int, chunk_images: int, src_dtype: int
 
 def approx_dct8x8_fused_sse_host(m: Matrix, src_host: torch.Tensor, r_list, workspace: torch.Tensor,
                                  chunk_images: int, clip: int = CLIP_NONE, sse_host: torch.Tensor | None = None,
-                                 stream=None) -> torch.Tensor:
-    """The fused path on a HOST image stack (pinned); returns host SSE [n, n_r]."""
+                                 stream=None, psnr_host: torch.Tensor | None = None, return_psnr: bool = False):
+    """The fused path on a HOST image stack (pinned); returns host SSE [n, n_r], or (sse, psnr)
+    with `psnr_host` / return_psnr=True."""
     g = geom_of(src_host)
     rl = [int(r) for r in r_list]
     arr = (ctypes.c_int32 * len(rl))(*rl)
     if sse_host is None:
         sse_host = torch.empty((g.n_images, len(rl)), dtype=torch.float64)
     _out(sse_host, g.n_images * len(rl), src_host, "sse_host", dtype=torch.float64, host=True)
+    want_psnr = return_psnr or psnr_host is not None
+    if want_psnr and psnr_host is None:
+        psnr_host = torch.empty((g.n_images, len(rl)), dtype=torch.float64)
+    if want_psnr:
+        _out(psnr_host, g.n_images * len(rl), src_host, "psnr_host", dtype=torch.float64, host=True)
     _check(lib.approx_dct8x8_fused_sse_host(m.handle, src_host.data_ptr(), dtype_code(src_host), g,
                                             ctypes.cast(arr, ctypes.c_void_p), len(rl), int(clip),
-                                            sse_host.data_ptr(), int(chunk_images), workspace.data_ptr(),
-                                            workspace.numel(), _stream_ptr(stream)), "approx_dct8x8_fused_sse_host")
-    return sse_host
+                                            sse_host.data_ptr(), psnr_host.data_ptr() if want_psnr else None,
+                                            int(chunk_images), workspace.data_ptr(), workspace.numel(),
+                                            _stream_ptr(stream)), "approx_dct8x8_fused_sse_host")
+    return (sse_host, psnr_host) if want_psnr else sse_host
 
 
 def approx_dct8x8_fwd_quant(m: Matrix, src: torch.Tensor, step: int = 16, q: torch.Tensor | None = None,
@@ -423,9 +441,3 @@ def approx_dct8x8_fwd_quant(m: Matrix, src: torch.Tensor, step: int = 16, q: tor
     _check(lib.approx_dct8x8_fwd_quant(m.handle, src.data_ptr(), g, int(step), q.data_ptr(), _stream_ptr(stream)),
            "approx_dct8x8_fwd_quant")
     return q
-
-
-def psnr_from_sse(sse: torch.Tensor, n_pixels: int, peak: float = 255.0) -> torch.Tensor:
-    """10 log10(peak^2 / (sse / n_pixels)); +inf where sse == 0 (host-side report helper)."""
-    mse = sse / float(n_pixels)
-    return torch.where(sse == 0, torch.full_like(sse, float("inf")), 10.0 * torch.log10(peak * peak / mse))

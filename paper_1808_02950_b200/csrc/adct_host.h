@@ -2,6 +2,7 @@
 #pragma once
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "adct.h"
 #include "adct_internal.cuh"
@@ -24,6 +25,22 @@ namespace adct {
 extern std::atomic<int64_t> g_launches;
 
 inline void count_launch(int64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Function attributes, __constant__ data, streams and SM counts are per device: everything the
+// library sets up lazily is keyed by the current device (cudaGetDevice), so a process that
+// calls it on cuda:1 after cuda:0 gets its own setup there.
+constexpr int kMaxDevices = 64;
+int device_sms();  // SM count of the current device (basic.cu), 148 on B200
+// Run f() (returning bool) once per device; the result is remembered, so a failed setup keeps
+// failing.  false also when the current device cannot be determined.
+template <class F>
+inline bool once_per_device(std::mutex& mu, int8_t (&state)[kMaxDevices], F&& f) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (state[dev] == 0) state[dev] = f() ? 1 : -1;
+  return state[dev] == 1;
+}
 
 inline adct_status check_geom(const adct_geom& g) {
   if (g.n_images < 0 || g.height <= 0 || g.width <= 0) return ADCT_E_INVALID_ARGUMENT;

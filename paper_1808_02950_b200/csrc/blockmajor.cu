@@ -337,28 +337,20 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
   if (lane == 0) bulk_wait<0>();
 }
 
-int g_bm_sms = 0;
-int bm_sms() {
-  if (!g_bm_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_bm_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_bm_sms <= 0) g_bm_sms = 148;
-  }
-  return g_bm_sms;
-}
+int bm_sms() { return device_sms(); }
 
 template <class MP, bool F32OUT>
 adct_status launch_rt_bm(const CUtensorMap& tin, const CUtensorMap& tout, const DevMat& dm, const Wk& wk,
                          uint32_t n_tiles, int clip, float lo, float hi, cudaStream_t st) {
   constexpr int kBmWarps = bm_warps<F32OUT>();
   constexpr size_t smem = (size_t)kBmWarps * (kBmInSlots * 4096 + (F32OUT ? 8192 : 4096)) + kBmWarps * kBmInSlots * 8 + 1024;
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [&] {
-    err = cudaFuncSetAttribute(roundtrip_bm_kernel<MP, F32OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
-  if (err != cudaSuccess) return ADCT_E_CUDA;
+  static std::mutex mu;
+  static int8_t state[kMaxDevices] = {};
+  if (!once_per_device(mu, state, [&] {
+        return cudaFuncSetAttribute(roundtrip_bm_kernel<MP, F32OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess;
+      }))
+    return ADCT_E_CUDA;
   const uint32_t need = (n_tiles + kBmWarps - 1) / kBmWarps;
   const unsigned grid = (unsigned)(need < (uint32_t)bm_sms() ? need : (uint32_t)bm_sms());
   roundtrip_bm_kernel<MP, F32OUT><<<grid, 32 * kBmWarps, smem, st>>>(tin, tout, dm, wk, n_tiles, clip, lo, hi);
@@ -369,12 +361,13 @@ template <int TW>
 adct_status launch_quant(const CUtensorMap& tin, const CUtensorMap& tout, const QTab& qt, float stepf, int32_t tpb,
                          int32_t tpi, int32_t bh, uint32_t n_tiles, cudaStream_t st) {
   constexpr size_t smem = (size_t)kQWarps * (kQInSlots * 4096 + 8192) + kQWarps * kQInSlots * 8 + 1024;
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [&] {
-    err = cudaFuncSetAttribute(fwd_quant_tma_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
-  if (err != cudaSuccess) return ADCT_E_CUDA;
+  static std::mutex mu;
+  static int8_t state[kMaxDevices] = {};
+  if (!once_per_device(mu, state, [&] {
+        return cudaFuncSetAttribute(fwd_quant_tma_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem) == cudaSuccess;
+      }))
+    return ADCT_E_CUDA;
   const uint32_t need = (n_tiles + kQWarps - 1) / kQWarps;
   const unsigned grid = (unsigned)(need < (uint32_t)bm_sms() ? need : (uint32_t)bm_sms());
   fwd_quant_tma_kernel<TW><<<grid, 32 * kQWarps, smem, st>>>(tin, tout, qt, stepf, tpb, tpi, bh, n_tiles,

@@ -18,13 +18,13 @@ namespace adct {
 
 void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
                      int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st);
-void launch_sweep_any(bool u8, bool specialized, int clip, cudaStream_t st, const void* src, const adct_geom& g,
+bool launch_sweep_any(bool u8, bool specialized, int clip, cudaStream_t st, const void* src, const adct_geom& g,
                       const KGeom& kg, const DevMat& dm, const FastDiv& dbw, uint64_t rmask, int32_t rmin,
                       double* partial);
 int64_t sweep_chunks(const adct_geom& g);
 bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t step, int16_t* q,
                    cudaStream_t st, adct_status* status);
-bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
+bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
                      double* partial, cudaStream_t st, adct_status* status);
 
 namespace {
@@ -151,16 +151,7 @@ __global__ void __launch_bounds__(256) fwd_quant_kernel(const uint8_t* __restric
   }
 }
 
-int g_sms = 0;
-int sms() {
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
-  }
-  return g_sms;
-}
+int sms() { return device_sms(); }
 
 // single-r kernels compiled in: (matrix, r) pairs of the benchmark configurations
 template <typename SrcT, class MP, int CLIP>
@@ -181,7 +172,7 @@ bool launch_single(int r, dim3 grid, cudaStream_t st, const SrcT* src, const KGe
 
 template <typename SrcT, class MP>
 adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geom& g, const int32_t* r_list,
-                           int32_t n_r, adct_clip clip, double* sse, double* partial, cudaStream_t st) {
+                           int32_t n_r, adct_clip clip, double* sse, double* psnr, double* partial, cudaStream_t st) {
   const KGeom kg = make_kgeom(g);
   const FastDiv dbw = make_fastdiv(kg.bw);
   int32_t chunks = (int32_t)fused_chunks(g);
@@ -192,7 +183,7 @@ adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geo
     if constexpr (std::is_same<SrcT, uint8_t>::value) {
       if (clip == ADCT_CLIP_NONE && m->is_int && !g_disable_stream) {
         adct_status stt = ADCT_OK;
-        if (fused_u8_stream(m, (const uint8_t*)src, g, r_list[0], sse, partial, st, &stt)) return stt;
+        if (fused_u8_stream(m, (const uint8_t*)src, g, r_list[0], sse, psnr, partial, st, &stt)) return stt;
       }
     }
     dim3 grid((unsigned)chunks, (unsigned)g.n_images);
@@ -211,14 +202,15 @@ adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geo
       if (r_list[i] < rmin) rmin = r_list[i];
       sm.s[i] = r_list[i] - 1;
     }
-    launch_sweep_any(std::is_same<SrcT, uint8_t>::value, MP::kConst, (int)clip, st, s, g, kg, m->dev, dbw, rmask,
-                     rmin, partial);
+    if (!launch_sweep_any(std::is_same<SrcT, uint8_t>::value, MP::kConst, (int)clip, st, s, g, kg, m->dev, dbw,
+                          rmask, rmin, partial))
+      return ADCT_E_CUDA;
     chunks = (int32_t)sweep_chunks(g);
     slots = 64;
   }
   count_launch();
   if (adct_status e = launch_status()) return e;
-  launch_finalize(partial, chunks, g.n_images, slots, sm, n_r, (double)g.height * g.width, 255.0, sse, nullptr, st);
+  launch_finalize(partial, chunks, g.n_images, slots, sm, n_r, (double)g.height * g.width, 255.0, sse, psnr, st);
   return launch_status();
 }
 
@@ -236,24 +228,26 @@ adct_status fused_check(const adct_matrix* m, const void* src, adct_dtype src_t,
 }
 
 adct_status fused_run(const adct_matrix* m, const void* src, adct_dtype src_t, const adct_geom& g,
-                      const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse, double* partial,
+                      const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse, double* psnr, double* partial,
                       cudaStream_t st) {
   if (g.n_images == 0) return ADCT_OK;
   if (src_t == ADCT_U8) {
-    if (m->specialized) return fused_dispatch<uint8_t, T1Mat>(m, src, g, r_list, n_r, clip, sse, partial, st);
-    return fused_dispatch<uint8_t, RtMat>(m, src, g, r_list, n_r, clip, sse, partial, st);
+    if (m->specialized) return fused_dispatch<uint8_t, T1Mat>(m, src, g, r_list, n_r, clip, sse, psnr, partial, st);
+    return fused_dispatch<uint8_t, RtMat>(m, src, g, r_list, n_r, clip, sse, psnr, partial, st);
   }
-  if (m->specialized) return fused_dispatch<int16_t, T1Mat>(m, src, g, r_list, n_r, clip, sse, partial, st);
-  return fused_dispatch<int16_t, RtMat>(m, src, g, r_list, n_r, clip, sse, partial, st);
+  if (m->specialized) return fused_dispatch<int16_t, T1Mat>(m, src, g, r_list, n_r, clip, sse, psnr, partial, st);
+  return fused_dispatch<int16_t, RtMat>(m, src, g, r_list, n_r, clip, sse, psnr, partial, st);
 }
 
-// copy stream of the host-buffer pipeline (one per process/device, created on first use)
+// copy stream of the host-buffer pipeline (one per device, created on first use there)
 cudaStream_t copy_stream() {
   static std::mutex mu;
-  static cudaStream_t s = nullptr;
+  static cudaStream_t s[kMaxDevices] = {};
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
-  if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-  return s;
+  if (!s[dev] && cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking) != cudaSuccess) s[dev] = nullptr;
+  return s[dev];
 }
 
 }  // namespace
@@ -264,46 +258,61 @@ using namespace adct;
 extern "C" {
 
 adct_status approx_dct8x8_fused_sse(const adct_matrix* m, const void* src, adct_dtype src_t, adct_geom g,
-                                    const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse,
+                                    const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse, double* psnr,
                                     void* workspace, size_t workspace_bytes, void* stream) {
   if (adct_status s = fused_check(m, src, src_t, g, r_list, n_r, clip)) return s;
   if (!sse) return ADCT_E_INVALID_ARGUMENT;
   if (!workspace || workspace_bytes < adct_workspace_bytes(g, n_r) || !aligned(workspace, 8)) return ADCT_E_WORKSPACE;
-  return fused_run(m, src, src_t, g, r_list, n_r, clip, sse, (double*)workspace, (cudaStream_t)stream);
+  return fused_run(m, src, src_t, g, r_list, n_r, clip, sse, psnr, (double*)workspace, (cudaStream_t)stream);
 }
 
-size_t adct_host_workspace_bytes(adct_geom g, int32_t n_r, int64_t chunk_images, adct_dtype src_t) {
+namespace {
+// Layout of the host-buffer pipeline's device workspace: two staging buffers of chunk_images
+// dense planes (the host stack is dense: image_stride = H * row_stride, whatever g says for a
+// single image), two partial buffers, then the SSE and PSNR tables [n_images][n_r].
+struct HostWs {
+  size_t stage, part, out;
+};
+HostWs host_ws(const adct_geom& g, int32_t n_r, int64_t chunk_images, adct_dtype src_t) {
   if (chunk_images < 1) chunk_images = 1;
   adct_geom gc = g;
   gc.n_images = chunk_images;
+  gc.image_stride = (int64_t)g.height * g.row_stride;
   const size_t esz = src_t == ADCT_I16 ? 2 : 1;
-  const size_t stage = ((size_t)chunk_images * (size_t)g.image_stride * esz + 255) / 256 * 256;
-  const size_t part = (adct_workspace_bytes(gc, n_r) + 255) / 256 * 256;
-  const size_t out = ((size_t)(g.n_images > 0 ? g.n_images : 0) * (size_t)(n_r > 0 ? n_r : 1) * sizeof(double) + 255) / 256 * 256;
-  return 2 * stage + 2 * part + out;
+  HostWs w;
+  w.stage = ((size_t)chunk_images * (size_t)gc.image_stride * esz + 255) / 256 * 256;
+  w.part = (adct_workspace_bytes(gc, n_r) + 255) / 256 * 256;
+  w.out = ((size_t)(g.n_images > 0 ? g.n_images : 0) * (size_t)(n_r > 0 ? n_r : 1) * sizeof(double) + 255) / 256 * 256;
+  return w;
+}
+}  // namespace
+
+size_t adct_host_workspace_bytes(adct_geom g, int32_t n_r, int64_t chunk_images, adct_dtype src_t) {
+  if (g.height <= 0 || g.row_stride <= 0) return 0;
+  const HostWs w = host_ws(g, n_r, chunk_images, src_t);
+  return 2 * w.stage + 2 * w.part + 2 * w.out;
 }
 
 adct_status approx_dct8x8_fused_sse_host(const adct_matrix* m, const void* src_host, adct_dtype src_t, adct_geom g,
                                          const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse_host,
-                                         int64_t chunk_images, void* workspace, size_t workspace_bytes,
-                                         void* stream) {
+                                         double* psnr_host, int64_t chunk_images, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
   if (adct_status s = fused_check(m, src_host, src_t, g, r_list, n_r, clip)) return s;
   if (!sse_host || chunk_images < 1) return ADCT_E_INVALID_ARGUMENT;
   if (g.n_images > 1 && g.image_stride != (int64_t)g.height * g.row_stride) return ADCT_E_INVALID_ARGUMENT;
   if (!workspace || workspace_bytes < adct_host_workspace_bytes(g, n_r, chunk_images, src_t)) return ADCT_E_WORKSPACE;
   if (g.n_images == 0) return ADCT_OK;
+  g.image_stride = (int64_t)g.height * g.row_stride;  // dense host stack (a lone image's stride is unused)
   cudaStream_t cs = (cudaStream_t)stream;
   cudaStream_t xs = copy_stream();
   if (!xs) return ADCT_E_CUDA;
-  adct_geom gc = g;
-  gc.n_images = chunk_images;
+  const HostWs w = host_ws(g, n_r, chunk_images, src_t);
   const size_t esz = src_t == ADCT_I16 ? 2 : 1;
-  const size_t stage = ((size_t)chunk_images * (size_t)g.image_stride * esz + 255) / 256 * 256;
-  const size_t part = (adct_workspace_bytes(gc, n_r) + 255) / 256 * 256;
   char* ws = (char*)workspace;
-  char* stg[2] = {ws, ws + stage};
-  double* prt[2] = {(double*)(ws + 2 * stage), (double*)(ws + 2 * stage + part)};
-  double* dsse = (double*)(ws + 2 * stage + 2 * part);
+  char* stg[2] = {ws, ws + w.stage};
+  double* prt[2] = {(double*)(ws + 2 * w.stage), (double*)(ws + 2 * w.stage + w.part)};
+  double* dsse = (double*)(ws + 2 * w.stage + 2 * w.part);
+  double* dpsnr = psnr_host ? (double*)(ws + 2 * w.stage + 2 * w.part + w.out) : nullptr;
   cudaEvent_t copied[2], freed[2];
   for (int i = 0; i < 2; ++i) {
     if (cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming) != cudaSuccess) return ADCT_E_CUDA;
@@ -317,7 +326,7 @@ adct_status approx_dct8x8_fused_sse_host(const adct_matrix* m, const void* src_h
   for (int64_t i0 = 0; i0 < g.n_images && st == ADCT_OK; i0 += chunk_images, ++c) {
     const int b = (int)(c & 1);
     const int64_t n = (g.n_images - i0) < chunk_images ? (g.n_images - i0) : chunk_images;
-    const size_t bytes = (size_t)((n - 1) * g.image_stride + (int64_t)g.height * g.row_stride) * esz;
+    const size_t bytes = (size_t)(n * g.image_stride) * esz;
     cudaStreamWaitEvent(xs, freed[b], 0);
     if (cudaMemcpyAsync(stg[b], (const char*)src_host + (size_t)i0 * g.image_stride * esz, bytes,
                         cudaMemcpyHostToDevice, xs) != cudaSuccess) { st = ADCT_E_CUDA; break; }
@@ -325,12 +334,14 @@ adct_status approx_dct8x8_fused_sse_host(const adct_matrix* m, const void* src_h
     cudaStreamWaitEvent(cs, copied[b], 0);
     adct_geom gi = g;
     gi.n_images = n;
-    st = fused_run(m, stg[b], src_t, gi, r_list, n_r, clip, dsse + i0 * n_r, prt[b], cs);
+    st = fused_run(m, stg[b], src_t, gi, r_list, n_r, clip, dsse + i0 * n_r, dpsnr ? dpsnr + i0 * n_r : nullptr,
+                   prt[b], cs);
     cudaEventRecord(freed[b], cs);
   }
-  if (st == ADCT_OK &&
-      cudaMemcpyAsync(sse_host, dsse, (size_t)g.n_images * n_r * sizeof(double), cudaMemcpyDeviceToHost, cs) !=
-          cudaSuccess)
+  const size_t tab = (size_t)g.n_images * n_r * sizeof(double);
+  if (st == ADCT_OK && cudaMemcpyAsync(sse_host, dsse, tab, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+    st = ADCT_E_CUDA;
+  if (st == ADCT_OK && dpsnr && cudaMemcpyAsync(psnr_host, dpsnr, tab, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
     st = ADCT_E_CUDA;
   if (cudaStreamSynchronize(cs) != cudaSuccess) st = ADCT_E_CUDA;
   for (int i = 0; i < 2; ++i) {

@@ -13,7 +13,9 @@
 //                   so both sides take every argmax decision on identical values;
 //  - search_kernel: per step, each thread scans a strided share of D, tests orthogonality with
 //                   the placed rows by DP4A on the packed digits, and keeps the best
-//                   (score, -index); the CTA reduction of that total order is deterministic.
+//                   (score, -index) and how many candidates share that score; the CTA
+//                   reduction of that total order is deterministic, and the tie counts of
+//                   equal scores add up, so exact ties (A22) are reported per sequence.
 #include <cmath>
 #include <utility>
 
@@ -91,10 +93,13 @@ __device__ __forceinline__ bool rows_placed_before(const int32_t*, int k, uint32
 __global__ void __launch_bounds__(kGrNT) search_kernel(const int8_t* __restrict__ digits, const double* __restrict__ score,
                                                       uint32_t n_vec, Fixed fx, uint32_t fixed_mask,
                                                       const int32_t* __restrict__ orders, int32_t n_free,
-                                                      int32_t* __restrict__ out, int32_t* __restrict__ status) {
+                                                      int32_t* __restrict__ out, int32_t* __restrict__ status,
+                                                      int32_t* __restrict__ ties) {
   __shared__ uint2 placed[8];
   __shared__ double best_s[kGrNT / 32];
   __shared__ uint32_t best_i[kGrNT / 32];
+  __shared__ uint32_t best_n[kGrNT / 32];
+  __shared__ int32_t tie[4];  // steps with a tie, first tied row, its tie size, largest tie size
   __shared__ int32_t rows[64];
   __shared__ int n_placed;
   const int order = blockIdx.x;
@@ -111,6 +116,10 @@ __global__ void __launch_bounds__(kGrNT) search_kernel(const int8_t* __restrict_
       if ((fixed_mask >> k) & 1u) placed[np++] = make_uint2(lo, hi);
     }
     n_placed = np;
+    tie[0] = 0;
+    tie[1] = -1;
+    tie[2] = 0;
+    tie[3] = 0;
   }
   __syncthreads();
   int32_t st = 0;
@@ -125,7 +134,7 @@ __global__ void __launch_bounds__(kGrNT) search_kernel(const int8_t* __restrict_
 #pragma unroll
     for (int p = 0; p < 8; ++p) pr[p] = p < np ? placed[p] : make_uint2(0u, 0u);
     double bs = -INFINITY;
-    uint32_t bi = 0xffffffffu;
+    uint32_t bi = 0xffffffffu, bn = 0;  // best score, its first index, candidates at that score
     const double* sk = score + (size_t)k * n_vec;
     for (uint32_t i = threadIdx.x; i < n_vec; i += kGrNT) {
       const uint2 w = reinterpret_cast<const uint2*>(digits)[i];
@@ -139,6 +148,9 @@ __global__ void __launch_bounds__(kGrNT) search_kernel(const int8_t* __restrict_
       if (s > bs) {  // strided scan visits i in increasing order: the first maximum is kept
         bs = s;
         bi = i;
+        bn = 1;
+      } else if (s == bs) {
+        ++bn;
       }
     }
     // CTA argmax of (score, -index): a total order, so the reduction order does not matter
@@ -146,24 +158,42 @@ __global__ void __launch_bounds__(kGrNT) search_kernel(const int8_t* __restrict_
     for (int o = 16; o > 0; o >>= 1) {
       const double os = __shfl_xor_sync(0xffffffffu, bs, o);
       const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (os > bs || (os == bs && oi < bi)) {
+      const uint32_t on = __shfl_xor_sync(0xffffffffu, bn, o);
+      if (os > bs) {
         bs = os;
         bi = oi;
+        bn = on;
+      } else if (os == bs) {
+        bi = oi < bi ? oi : bi;
+        bn += on;
       }
     }
     if ((threadIdx.x & 31) == 0) {
       best_s[threadIdx.x >> 5] = bs;
       best_i[threadIdx.x >> 5] = bi;
+      best_n[threadIdx.x >> 5] = bn;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = best_s[0];
-      uint32_t idx = best_i[0];
+      uint32_t idx = best_i[0], cnt = best_n[0];
       for (int q = 1; q < kGrNT / 32; ++q)
-        if (best_s[q] > s || (best_s[q] == s && best_i[q] < idx)) {
+        if (best_s[q] > s) {
           s = best_s[q];
           idx = best_i[q];
+          cnt = best_n[q];
+        } else if (best_s[q] == s) {
+          idx = best_i[q] < idx ? best_i[q] : idx;
+          cnt += best_n[q];
         }
+      if (idx != 0xffffffffu && cnt > 1) {  // an exact tie: the earliest vector was taken (A22)
+        if (tie[0] == 0) {
+          tie[1] = k;
+          tie[2] = (int32_t)cnt;
+        }
+        ++tie[0];
+        tie[3] = (int32_t)cnt > tie[3] ? (int32_t)cnt : tie[3];
+      }
       if (idx == 0xffffffffu) {
         n_placed = -1;  // infeasible
       } else {
@@ -182,6 +212,7 @@ __global__ void __launch_bounds__(kGrNT) search_kernel(const int8_t* __restrict_
   for (int t = threadIdx.x; t < 64; t += kGrNT) out[(size_t)order * 64 + t] = st ? 0 : rows[t];
   // status: 0 ok, 1 infeasible (no orthogonal candidate left), 2 invalid sequence
   if (threadIdx.x == 0) status[order] = st;
+  if (ties && threadIdx.x < 4) ties[(size_t)order * 4 + threadIdx.x] = tie[threadIdx.x];
 }
 
 uint32_t ipow8(int32_t n) {
@@ -205,7 +236,8 @@ size_t adct_greedy_workspace_bytes(int32_t n_entries) {
 
 adct_status adct_greedy_search(const double c[64], const int32_t* entries, int32_t n_entries, const int32_t fixed[64],
                                uint32_t fixed_mask, const int32_t* orders, int32_t n_orders, int32_t* out,
-                               int32_t* status, void* workspace, size_t workspace_bytes, void* stream) {
+                               int32_t* status, int32_t* ties, void* workspace, size_t workspace_bytes,
+                               void* stream) {
   if (!c || !entries || !orders || !out || !status || (fixed_mask && !fixed)) return ADCT_E_INVALID_ARGUMENT;
   if (n_entries < 1 || n_entries > 8 || n_orders < 0 || fixed_mask > 0xffu) return ADCT_E_INVALID_ARGUMENT;
   int32_t ent[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -235,7 +267,8 @@ adct_status adct_greedy_search(const double c[64], const int32_t* entries, int32
   score_kernel<<<g1, 256, 0, st>>>(digits, n_vec, cr, score);
   Fixed fx;
   for (int t = 0; t < 64; ++t) fx.t[t] = fixed_mask ? fixed[t] : 0;
-  search_kernel<<<(unsigned)n_orders, kGrNT, 0, st>>>(digits, score, n_vec, fx, fixed_mask, orders, n_free, out, status);
+  search_kernel<<<(unsigned)n_orders, kGrNT, 0, st>>>(digits, score, n_vec, fx, fixed_mask, orders, n_free, out, status,
+                                                     ties);
   count_launch(3);
   return launch_status();
 }

@@ -117,7 +117,12 @@ __device__ __forceinline__ void to_float(const RawRow<N, int16_t>& r, float* x) 
     const uint32_t w[4] = {r.v[c].x, r.v[c].y, r.v[c].z, r.v[c].w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      x[c * 8 + 2 * q] = (float)(int32_t)__byte_perm(w[q], 0u, 0x9910u);  // sign-extended low half
+      // low half sign-extended by PRMT's sign-replicate mode (selector nibble bit 3).  Written in
+      // PTX: __byte_perm uses only the low 3 bits of each nibble (it would COPY byte 1, which
+      // equals its sign fill only for |x| <= 255 -- found by the full int16-range test)
+      uint32_t lo;
+      asm("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(lo) : "r"(w[q]));
+      x[c * 8 + 2 * q] = (float)(int32_t)lo;
       x[c * 8 + 2 * q + 1] = (float)((int32_t)w[q] >> 16);
     }
   }

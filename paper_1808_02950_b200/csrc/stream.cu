@@ -39,15 +39,8 @@ bool make_u8_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int g_sms_s = 0;
 int sms_s() {
-  if (!g_sms_s) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms_s, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms_s <= 0) g_sms_s = 148;
-  }
-  return g_sms_s;
+  return device_sms();
 }
 
 namespace {
@@ -412,7 +405,7 @@ bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const 
 // The streaming path for (u8 source, integer matrix, no clip, one r); returns false when the
 // geometry or r is not covered (the caller then uses the generic fused kernels).
 // On success the per-image SSE is in sse[n_images] (finalize launched on st).
-bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
+bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
                  double* partial, cudaStream_t st, adct_status* status);
 
 // ADCT_HOT=simt selects this file's SIMT streaming kernel instead of the tensor-core one (tc.cu;
@@ -422,9 +415,9 @@ static const bool g_hot_simt = [] {
   return e && std::strcmp(e, "simt") == 0;
 }();
 
-bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
+bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
                      double* partial, cudaStream_t st, adct_status* status) {
-  if (!g_hot_simt && fused_u8_tc(m, src, g, r, sse, partial, st, status)) return true;
+  if (!g_hot_simt && fused_u8_tc(m, src, g, r, sse, psnr, partial, st, status)) return true;
   {
     WtPlan p = wt_plan(g);
     if (!p.ok || g.n_images == 0 || !aligned(src, 16)) return false;
@@ -455,7 +448,7 @@ bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& 
     SlotMap sm{};
     sm.s[0] = 0;
     launch_finalize(partial, p.cpi * kWtWarps, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0, sse,
-                    nullptr, st);
+                    psnr, st);
     *status = launch_status();
     return true;
   }

@@ -111,24 +111,28 @@ int64_t sweep_chunks(const adct_geom& g) {
   return (nbi + per - 1) / per;
 }
 
-void launch_sweep_any(bool u8, bool specialized, int clip, cudaStream_t st, const void* src, const adct_geom& g,
+bool launch_sweep_any(bool u8, bool specialized, int clip, cudaStream_t st, const void* src, const adct_geom& g,
                       const KGeom& kg, const DevMat& dm, const FastDiv& dbw, uint64_t rmask, int32_t rmin,
                       double* partial) {
   const int32_t chunks = (int32_t)sweep_chunks(g), bpt = sweep_bpt(g);
   const dim3 grid((unsigned)chunks, (unsigned)g.n_images);
   (void)specialized;
-  static bool zz_ready = [] {
-    int8_t zz[64];
-    for (int z = 0; z < 64; ++z) zz[z] = (int8_t)kZZ.order[z];
-    return cudaMemcpyToSymbol(c_zz, zz, sizeof(zz)) == cudaSuccess;
-  }();
-  (void)zz_ready;
+  // c_zz is __constant__ memory of the current device: uploaded once per device
+  static std::mutex mu;
+  static int8_t state[kMaxDevices] = {};
+  if (!once_per_device(mu, state, [] {
+        int8_t zz[64];
+        for (int z = 0; z < 64; ++z) zz[z] = (int8_t)kZZ.order[z];
+        return cudaMemcpyToSymbol(c_zz, zz, sizeof(zz)) == cudaSuccess;
+      }))
+    return false;
   if (u8)
     fused_sweep_kernel<uint8_t><<<grid, NT, 0, st>>>((const uint8_t*)src, kg, dm, dbw, chunks, bpt, rmask, rmin, clip,
                                                      partial);
   else
     fused_sweep_kernel<int16_t><<<grid, NT, 0, st>>>((const int16_t*)src, kg, dm, dbw, chunks, bpt, rmask, rmin, clip,
                                                      partial);
+  return true;
 }
 
 }  // namespace adct

@@ -465,7 +465,7 @@ TcPlan tc_plan(const adct_geom& g) {
 
 // The tensor-core streaming path for (u8 source, integer matrix, no clip, one r); false when
 // the geometry or r is not covered (the caller then uses the SIMT streaming kernel).
-bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse,
+bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
                  double* partial, cudaStream_t st, adct_status* status) {
   const TcPlan p = tc_plan(g);
   if (!p.ok || g.n_images == 0 || !aligned(src, 16) || !m->is_int) return false;
@@ -485,7 +485,7 @@ bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, i
   if ((*status = launch_status()) != ADCT_OK) return true;
   SlotMap sm{};
   sm.s[0] = 0;
-  launch_finalize(partial, p.cpi * kTcPartials, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0, sse, nullptr,
+  launch_finalize(partial, p.cpi * kTcPartials, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0, sse, psnr,
                   st);
   *status = launch_status();
   return true;

@@ -59,25 +59,58 @@ class ErrorTable:
     result is bit-identical to a single-process run however often it is combined.  (All-reducing
     the output in place step after step would add the other ranks' stale copies.)  Storage is
     column-major, so `out(col)` -- this rank's rows of one column -- is contiguous and a kernel
-    writes its per-image results there directly; `local` and `table` are [n_total, cols] views."""
+    writes its per-image results there directly; `local` and `table` are [n_total, cols] views.
 
-    def __init__(self, n_total: int, cols: int, lo: int, hi: int, device=None):
+    With buffers=2 and a side stream, step k writes buffer k % 2 while the previous step's
+    buffer is copied and all-reduced on the side stream (`combine(buf, stream=side)`), so the
+    collective overlaps the next step's kernels; `before_write(buf)` orders the rewrite of a
+    buffer after its last copy and `wait(buf)` orders the current stream after its all-reduce."""
+
+    def __init__(self, n_total: int, cols: int, lo: int, hi: int, device=None, buffers: int = 1):
         self.lo, self.hi = lo, hi
-        self._local = torch.zeros((cols, n_total), dtype=torch.float64, device=device)
+        self._local = torch.zeros((buffers, cols, n_total), dtype=torch.float64, device=device)
         self._table = torch.zeros_like(self._local)
-        self.local = self._local.t()
-        self.table = self._table.t()
+        self._copied = [None] * buffers
+        self._done = [None] * buffers
+        self.local = self._local[0].t()
+        self.table = self._table[0].t()
 
-    def out(self, col: int) -> torch.Tensor:
-        return self._local[col, self.lo:self.hi]
+    def out(self, col: int, buf: int = 0) -> torch.Tensor:
+        return self._local[buf, col, self.lo:self.hi]
 
-    def set_local(self, col: int, values: torch.Tensor) -> None:
-        self.out(col).copy_(values.reshape(self.hi - self.lo))
+    def local_of(self, buf: int) -> torch.Tensor:
+        return self._local[buf].t()
 
-    def combine(self) -> torch.Tensor:
-        self._table.copy_(self._local)
-        combine_error_table(self._table)
-        return self.table
+    def table_of(self, buf: int) -> torch.Tensor:
+        return self._table[buf].t()
+
+    def set_local(self, col: int, values: torch.Tensor, buf: int = 0) -> None:
+        self.out(col, buf).copy_(values.reshape(self.hi - self.lo))
+
+    def combine(self, buf: int = 0, stream=None) -> torch.Tensor:
+        if stream is None:
+            self._table[buf].copy_(self._local[buf])
+            combine_error_table(self._table[buf])
+            return self.table_of(buf)
+        cur = torch.cuda.current_stream(self._local.device)
+        stream.wait_stream(cur)  # after the kernels that wrote this buffer
+        if self._copied[buf] is None:
+            self._copied[buf] = torch.cuda.Event()
+            self._done[buf] = torch.cuda.Event()
+        with torch.cuda.stream(stream):
+            self._table[buf].copy_(self._local[buf])
+            self._copied[buf].record(stream)
+            combine_error_table(self._table[buf])
+            self._done[buf].record(stream)
+        return self.table_of(buf)
+
+    def before_write(self, buf: int) -> None:
+        if self._copied[buf] is not None:
+            torch.cuda.current_stream(self._local.device).wait_event(self._copied[buf])
+
+    def wait(self, buf: int) -> None:
+        if self._done[buf] is not None:
+            torch.cuda.current_stream(self._local.device).wait_event(self._done[buf])
 
 
 def combine_error_table(local: torch.Tensor) -> torch.Tensor:

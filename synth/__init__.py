@@ -80,15 +80,23 @@ def ar1_field(n: int, h: int, w: int, rho, mean=128.0, std=40.0, seed: int = 1, 
 
 
 def ar1_stack(n: int, h: int, w: int, rho, mean=128.0, std=40.0, seed: int = 1, device="cpu",
-              noise_uniform: float = 0.0, batch: int = 16) -> torch.Tensor:
-    """Large stacks generated in batches of images (seed + batch index) to bound memory."""
-    out = torch.empty((n, h, w), dtype=torch.uint8, device=device)
+              noise_uniform: float = 0.0, batch: int = 16, lo: int = 0, hi: int | None = None) -> torch.Tensor:
+    """Large stacks generated in batches of images (seed + batch start) to bound memory.
+
+    lo/hi select frames [lo, hi) of the n-frame stack without generating the others (batches
+    stay aligned to global multiples of `batch`), so a rank's shard of a sharded stack is
+    bit-identical to the same frames of the whole stack."""
+    hi = n if hi is None else hi
+    if not (0 <= lo <= hi <= n):
+        raise ValueError("bad frame range")
+    out = torch.empty((hi - lo, h, w), dtype=torch.uint8, device=device)
     rho_a = np.broadcast_to(np.asarray(rho, dtype=np.float64), (n,))
     std_a = np.broadcast_to(np.asarray(std, dtype=np.float64), (n,))
-    for b0 in range(0, n, batch):
+    for b0 in range(lo - lo % batch, hi, batch):
         b1 = min(n, b0 + batch)
-        out[b0:b1] = ar1_field(b1 - b0, h, w, rho_a[b0:b1], mean, std_a[b0:b1], seed * 100003 + b0, device,
-                               noise_uniform)
+        f = ar1_field(b1 - b0, h, w, rho_a[b0:b1], mean, std_a[b0:b1], seed * 100003 + b0, device, noise_uniform)
+        a, b = max(lo, b0), min(hi, b1)
+        out[a - lo:b - lo] = f[a - b0:b - b0]
     return out
 
 
@@ -101,11 +109,12 @@ def config2_params(n: int = 45, master_seed: int = 2):
 
 
 def yuv420_stack(n_frames: int, height: int = 2160, width: int = 3840, seed: int = 4, device="cpu",
-                 batch: int = 8):
-    """Config 4: luma AR(1) rho=0.95, chroma (half resolution) rho=0.9 (reading A14)."""
-    y = ar1_stack(n_frames, height, width, 0.95, 128.0, 40.0, seed, device, batch=batch)
-    u = ar1_stack(n_frames, height // 2, width // 2, 0.90, 128.0, 40.0, seed + 1, device, batch=batch)
-    v = ar1_stack(n_frames, height // 2, width // 2, 0.90, 128.0, 40.0, seed + 2, device, batch=batch)
+                 batch: int = 8, lo: int = 0, hi: int | None = None):
+    """Config 4: luma AR(1) rho=0.95, chroma (half resolution) rho=0.9 (reading A14); frames
+    [lo, hi) of the n_frames stack (default: all)."""
+    y = ar1_stack(n_frames, height, width, 0.95, 128.0, 40.0, seed, device, batch=batch, lo=lo, hi=hi)
+    u = ar1_stack(n_frames, height // 2, width // 2, 0.90, 128.0, 40.0, seed + 1, device, batch=batch, lo=lo, hi=hi)
+    v = ar1_stack(n_frames, height // 2, width // 2, 0.90, 128.0, 40.0, seed + 2, device, batch=batch, lo=lo, hi=hi)
     return y, u, v
 
 
@@ -120,6 +129,26 @@ def laplace_blocks(n_blocks: int, scale: float = 10.0, seed: int = 5, device="cp
     x = -scale * torch.sign(u) * torch.log1p(-2.0 * u.abs())
     x = torch.sign(x) * torch.floor(x.abs() + 0.5)
     return x.clamp(-255, 255).to(torch.int16)
+
+
+LAPLACE_BATCH = 1 << 22  # blocks per generator batch of the large C5 sweeps
+
+
+def laplace_range(lo: int, hi: int, scale: float = 10.0, seed: int = 5, device="cpu",
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """Blocks [lo, hi) of the C5 block sequence (int16 [hi - lo, 8, 8]), generated in batches of
+    LAPLACE_BATCH blocks (seed + batch index) so that 2^30 blocks (137 GB) need only one batch
+    of temporaries and any contiguous shard equals the same blocks of the whole sequence."""
+    if not (0 <= lo <= hi):
+        raise ValueError("bad block range")
+    if out is None:
+        out = torch.empty((hi - lo, 8, 8), dtype=torch.int16, device=device)
+    B = LAPLACE_BATCH
+    for b0 in range(lo - lo % B, hi, B):
+        blk = laplace_blocks(B, scale, seed * 1000003 + b0 // B, device)
+        a, b = max(lo, b0), min(hi, b0 + B)
+        out[a - lo:b - lo] = blk[a - b0:b - b0]
+    return out
 
 
 def uniform_blocks_u8(n_img: int, h: int, w: int, seed: int = 7, device="cpu") -> torch.Tensor:

@@ -117,11 +117,20 @@ def test_argument_validation_before_launch():
     assert L.approx_dct8x8_inv(m.handle, fake, adct.I32, _fake(), fake, adct.U8, adct.CLIP_NONE, None) == 1
     rl = (adct.ctypes.c_int32 * 2)(10, 0)
     assert L.approx_dct8x8_fused_sse(m.handle, fake, adct.U8, _fake(), adct.ctypes.cast(rl, adct.ctypes.c_void_p),
-                                     2, 0, fake, fake, 1 << 30, None) == 1
+                                     2, 0, fake, None, fake, 1 << 30, None) == 1
     rl = (adct.ctypes.c_int32 * 1)(10)
     assert L.approx_dct8x8_fused_sse(m.handle, fake, adct.U8, _fake(), adct.ctypes.cast(rl, adct.ctypes.c_void_p),
-                                     1, 0, fake, fake, 8, None) == 7
+                                     1, 0, fake, fake, fake, 8, None) == 7
     assert L.psnr_reduce(fake, adct.U8, fake, adct.F32, _fake(), 0.0, 0, fake, fake, fake, 1 << 30, None) == 1
+
+
+def test_host_workspace_lone_image_stride():
+    """A lone image's image_stride is ignored by the host path: its workspace is sized
+    from H * row_stride, so image_stride = 0 and = H * row_stride give the same size."""
+    g0 = adct.Geom(1, 2160, 3840, 0, 3840)
+    g1 = adct.Geom(1, 2160, 3840, 2160 * 3840, 3840)
+    assert adct.host_workspace_bytes(g0, 1, 16) == adct.host_workspace_bytes(g1, 1, 16)
+    assert adct.host_workspace_bytes(g0, 1, 1) >= 2 * 2160 * 3840
 
 
 def test_workspace_sizes_monotone():
@@ -154,10 +163,10 @@ def test_argument_validation_next_rows():
     ep = adct.ctypes.cast(ent, adct.ctypes.c_void_p)
     dup = (adct.ctypes.c_int32 * 3)(-1, 0, 0)
     # greedy: no entries, duplicate entries, workspace too small
-    assert L.adct_greedy_search(cp, ep, 0, None, 0, fake, 1, fake, fake, fake, 1 << 30, None) == 1
+    assert L.adct_greedy_search(cp, ep, 0, None, 0, fake, 1, fake, fake, None, fake, 1 << 30, None) == 1
     assert L.adct_greedy_search(cp, adct.ctypes.cast(dup, adct.ctypes.c_void_p), 3, None, 0, fake, 1, fake, fake,
-                                fake, 1 << 30, None) == 1
-    assert L.adct_greedy_search(cp, ep, 3, None, 0, fake, 1, fake, fake, fake, 16, None) == 7
+                                None, fake, 1 << 30, None) == 1
+    assert L.adct_greedy_search(cp, ep, 3, None, 0, fake, 1, fake, fake, fake, fake, 16, None) == 7
     assert L.adct_greedy_workspace_bytes(3) >= 9 * 8 * 6561
     # JAM: block size, r range, geometry, alignment
     g16 = adct.Geom(1, 32, 32, 1024, 32)

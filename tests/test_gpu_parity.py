@@ -3,6 +3,7 @@ inputs.  Integer transform / retention / quantiser: bit-exact.  Floating point (
 inverse, error): <= 1e-5 relative (per-block max-norm for arrays; per value for SSE) and
 <= 1e-3 dB PSNR (BASELINE.json north_star); SSE exactly 0 where the oracle's is 0 (r = 64).
 """
+import ctypes
 import fractions
 import math
 
@@ -273,20 +274,54 @@ def test_config1_full_size(mats):
     """C1: one 512x512 AR(1) image, r = 1..64, T1 — every r against the oracle."""
     img = synth.ar1_field(1, 512, 512, 0.95, seed=1)
     rs = list(range(1, 65))
-    sse = adct.approx_dct8x8_fused_sse(mats["T1"], img.to(DEV), rs).cpu().numpy()
+    sse, psnr = adct.approx_dct8x8_fused_sse(mats["T1"], img.to(DEV), rs, return_psnr=True)
+    sse, psnr = sse.cpu().numpy(), psnr.cpu().numpy()
     ref = oracle.codec_sse(img.numpy(), rs, t=M.T1)
     _check_sse(sse, ref)
-    psnr = adct.psnr_from_sse(torch.from_numpy(sse), 512 * 512).numpy()
-    for r in (1, 3, 10, 63):
-        assert abs(psnr[0, r - 1] - oracle.psnr(ref[0, r - 1], 512 * 512)) <= 1e-3
+    for r in rs:  # the library's PSNR (finalize kernel), north star: <= 1e-3 dB
+        if r == 64:  # reading A8: SSE is exactly 0 and PSNR +inf (the fp64 oracle leaves ~1e-20)
+            assert sse[0, 63] == 0.0 and ref[0, 63] < 1e-6
+            assert math.isinf(psnr[0, 63]) and psnr[0, 63] > 0
+        else:
+            assert abs(psnr[0, r - 1] - oracle.psnr(ref[0, r - 1], 512 * 512)) <= 1e-3
 
 
 def test_config4_sampled_frames(mats):
-    """C4 geometry (3840x2160 luma, 1920x1080 chroma), hot kernel r = 10, on sampled frames."""
+    """C4 geometry (3840x2160 luma, 1920x1080 chroma), hot kernel r = 10, on sampled frames;
+    per-plane PSNR from the library within 1e-3 dB."""
     y, u, v = synth.yuv420_stack(2, seed=4)
     for plane in (y, u, v):
-        sse = adct.approx_dct8x8_fused_sse(mats["T1"], plane.to(DEV), [10]).cpu().numpy()
-        _check_sse(sse, oracle.codec_sse(plane.numpy(), [10], t=M.T1))
+        sse, psnr = adct.approx_dct8x8_fused_sse(mats["T1"], plane.to(DEV), [10], return_psnr=True)
+        ref = oracle.codec_sse(plane.numpy(), [10], t=M.T1)
+        _check_sse(sse.cpu().numpy(), ref)
+        npix = plane.shape[1] * plane.shape[2]
+        for i in range(plane.shape[0]):
+            assert abs(float(psnr[i, 0]) - oracle.psnr(ref[i, 0], npix)) <= 1e-3
+
+
+@pytest.mark.parametrize("r_list", [[10], [3, 10, 64]])
+def test_fused_host_psnr(mats, r_list):
+    """Host-buffer path: SSE and PSNR equal the device path's bit for bit; PSNR +inf at r = 64;
+    a lone image whose image_stride is 0 (ignored for one image) stages correctly."""
+    img = images("ar1", 5, 64, 128, seed=32)
+    dsse, dpsnr = adct.approx_dct8x8_fused_sse(mats["T1"], img.to(DEV), r_list, return_psnr=True)
+    host = img.pin_memory()
+    g = adct.geom_of(host)
+    ws = torch.empty(adct.host_workspace_bytes(g, len(r_list), 2), dtype=torch.uint8, device=DEV)
+    hsse, hpsnr = adct.approx_dct8x8_fused_sse_host(mats["T1"], host, r_list, ws, chunk_images=2, return_psnr=True)
+    assert torch.equal(hsse, dsse.cpu()) and torch.equal(hpsnr, dpsnr.cpu())
+    if 64 in r_list:
+        assert torch.all(hpsnr[:, r_list.index(64)] == float("inf"))
+    one = host[:1]
+    g1 = adct.geom_of(one)
+    g1.image_stride = 0
+    ws1 = torch.empty(adct.host_workspace_bytes(g1, len(r_list), 1), dtype=torch.uint8, device=DEV)
+    out = torch.empty((1, len(r_list)), dtype=torch.float64).pin_memory()
+    rl = (ctypes.c_int32 * len(r_list))(*r_list)
+    st = adct.lib.approx_dct8x8_fused_sse_host(mats["T1"].handle, one.data_ptr(), adct.U8, g1,
+                                               ctypes.cast(rl, ctypes.c_void_p), len(r_list), adct.CLIP_NONE,
+                                               out.data_ptr(), None, 1, ws1.data_ptr(), ws1.numel(), None)
+    assert st == 0 and torch.equal(out, dsse[:1].cpu())
 
 
 # --- quantiser ----------------------------------------------------------------------------------
@@ -450,6 +485,43 @@ def test_roundtrip_blockmajor_tma_path(mats, name, out):
         assert rel_block_err(rec, _oracle_recon(name, x.numpy(), 10)) <= RTOL
 
 
+def _check_int_recon(rec, ref, lo=-32768, hi=32767):
+    """Integer reconstruction (round half even, saturate) against the exact oracle value: equal,
+    or one level off only where the exact value is within 1e-3 of a .5 tie (fp32 rounding)."""
+    ref_i = np.clip(np.rint(ref), lo, hi)
+    diff = np.abs(rec.astype(np.int64) - ref_i)
+    assert diff.max() <= 1
+    assert np.all(np.abs(np.abs(ref - np.floor(ref)) - 0.5)[diff > 0] < 1e-3)
+
+
+@pytest.mark.parametrize("name", ["T1", "DCT", "T6"])
+@pytest.mark.parametrize("n_blocks", [32 * 97, 32 * 97 + 5])  # TMA block-major path / generic kernel
+def test_roundtrip_in_place(mats, name, n_blocks):
+    """C5 runs in place at 2^30 blocks (recon IS src): the same call with recon = src gives the
+    out-of-place result bit for bit -- r = 64 (the identity for T1 and C) and r = 10."""
+    x = synth.laplace_range(0, n_blocks, seed=9)
+    for r in (64, 10):
+        want = adct.approx_dct8x8_roundtrip(mats[name], x.to(DEV), r, torch.int16).cpu()
+        xd = x.to(DEV)
+        got = adct.approx_dct8x8_roundtrip(mats[name], xd, r, torch.int16, recon=xd)
+        assert got.data_ptr() == xd.data_ptr()
+        assert torch.equal(xd.cpu(), want)
+        if r == 64 and name in ("T1", "DCT"):
+            assert torch.equal(want, x)
+        idx = np.arange(0, n_blocks, 101)
+        _check_int_recon(want.numpy()[idx], _oracle_recon(name, x.numpy()[idx], r))
+
+
+def test_roundtrip_in_place_u8_images(mats):
+    """u8 images reconstructed in place (round half even, clip [0, 255]) equal out of place."""
+    img = images("ar1", 3, 72, 264, seed=12)
+    want = adct.approx_dct8x8_roundtrip(mats["T1"], img.to(DEV), 10, torch.uint8).cpu()
+    xd = img.to(DEV)
+    adct.approx_dct8x8_roundtrip(mats["T1"], xd, 10, torch.uint8, recon=xd)
+    assert torch.equal(xd.cpu(), want)
+    _check_int_recon(want.numpy(), _oracle_recon("T1", img.numpy(), 10), 0, 255)
+
+
 # --- SSIM (next row f1; reading A18) -------------------------------------------------------------
 
 from oracle import ssim as OS  # noqa: E402
@@ -553,6 +625,24 @@ def test_jam_roundtrip_int16_bit_exact_and_u8(n):
     assert np.all(np.abs(np.abs(ref - np.floor(ref)) - 0.5)[diff > 0] < 1e-3)
 
 
+@pytest.mark.parametrize("n", [16, 32])
+def test_jam_full_int16_range(n):
+    """Beyond |x| = 7281 the fp32 forward is no longer exact integer arithmetic (include/adct.h):
+    over the WHOLE int16 range (uniform, extremal +-32767/-32768 blocks) the fp32 round trip still
+    meets the north-star 1e-5 per-block bound against the fp64 oracle, and the int16 round trip
+    at r = n^2 is the identity (checked, not assumed: bit-exact here)."""
+    t = OJ.T16 if n == 16 else OJ.T32
+    g = torch.Generator().manual_seed(70 + n)
+    uni = torch.randint(-32768, 32768, (64, n, n), generator=g, dtype=torch.int32).to(torch.int16)
+    ext = (torch.randint(0, 2, (64, n, n), generator=g) * 65535 - 32768).to(torch.int16)  # -32768 / 32767
+    for x in (uni, ext):
+        for r in (10, n * n // 3, n * n):
+            rec = adct.approx_dct_jam_roundtrip(n, x.to(DEV), r, torch.float32).cpu().numpy()
+            assert _rel_err_nn(rec, OJ.recon_n(t, x.numpy(), r), n) <= RTOL, (n, r)
+        rec = adct.approx_dct_jam_roundtrip(n, x.to(DEV), n * n, torch.int16)
+        assert torch.equal(rec.cpu(), x)
+
+
 def test_jam_argument_errors():
     x = torch.zeros((1, 16, 16), dtype=torch.int16, device=DEV)
     with pytest.raises(adct.AdctError):
@@ -574,39 +664,66 @@ def greedy_spaces():
     return {1: OG.Search(OG.P1), 2: OG.Search(OG.P2)}
 
 
-@pytest.mark.parametrize("space", [1, 2])
-def test_greedy_search_fixed_rows_all_orders(greedy_spaces, space):
-    """§4.1 setting: rows 1 and 5 fixed, all 720 orders of the other six; every sequence's
-    matrix (or infeasibility) equals the oracle's; D2 yields exactly T1 and T2."""
-    s = greedy_spaces[space]
-    ref = s.derive_all()
-    orders = np.array([o for o, _ in ref], dtype=np.int32)
-    mats, status = adct.greedy_search(M.C, OG.P1 if space == 1 else OG.P2, orders, fixed=OG.FIXED_ROWS, device=DEV)
-    mats, status = mats.cpu().numpy(), status.cpu().numpy()
-    for n, (o, m) in enumerate(ref):
+def _tie_summary(ties):
+    """The oracle's logged ties of one sequence as the C-ABI reports them: (steps with a tie,
+    first tied row or -1, candidates tied there, largest tie)."""
+    if not ties:
+        return [0, -1, 0, 0]
+    return [len(ties), ties[0][1], len(ties[0][2]), max(len(t[2]) for t in ties)]
+
+
+def _check_search(s, entries, orders, fixed):
+    mats, status, ties = adct.greedy_search(M.C, entries, np.array(orders, dtype=np.int32), fixed=fixed, device=DEV,
+                                            return_ties=True)
+    mats, status, ties = mats.cpu().numpy(), status.cpu().numpy(), ties.cpu().numpy()
+    n_tied = 0
+    for n, o in enumerate(orders):
+        log = []
+        m = s.solve(tuple(o), fixed, ties=log)
         if m is None:
             assert status[n] == 1, o
         else:
             assert status[n] == 0 and np.array_equal(mats[n], m), o
+        assert ties[n].tolist() == _tie_summary(log), (o, log)
+        n_tied += bool(log)
+    return mats, status, n_tied
+
+
+@pytest.mark.parametrize("space", [1, 2])
+def test_greedy_search_fixed_rows_all_orders(greedy_spaces, space):
+    """§4.1 setting: rows 1 and 5 fixed, all 720 orders of the other six; every sequence's
+    matrix (or infeasibility) and its logged exact ties equal the oracle's; D2 yields exactly
+    T1 and T2."""
+    s = greedy_spaces[space]
+    free = [k for k in range(8) if k not in OG.FIXED_ROWS]
+    orders = list(_it.permutations(free))
+    mats, status, _ = _check_search(s, OG.P1 if space == 1 else OG.P2, orders, OG.FIXED_ROWS)
     if space == 2:
-        got = {mats[n].tobytes() for n in range(len(ref)) if status[n] == 0}
+        got = {mats[n].tobytes() for n in range(len(orders)) if status[n] == 0}
         assert got == {np.array(M.T1, dtype=np.int32).tobytes(), np.array(M.T2, dtype=np.int32).tobytes()}
 
 
 def test_greedy_search_free_orders_d1(greedy_spaces):
     """All eight rows free (§3.4): the worked forward/reverse orders and 62 sampled
-    permutations of 8! over D1, against the oracle."""
+    permutations of 8! over D1, against the oracle -- matrices and logged ties.  The reverse
+    order meets an exact tie (reading A22)."""
     s = greedy_spaces[1]
     rng = np.random.default_rng(7)
     perms = [tuple(range(8)), tuple(range(7, -1, -1))] + [tuple(rng.permutation(8)) for _ in range(62)]
-    mats, status = adct.greedy_search(M.C, OG.P1, np.array(perms, dtype=np.int32), device=DEV)
-    mats, status = mats.cpu().numpy(), status.cpu().numpy()
-    for n, p in enumerate(perms):
-        m = s.solve(p)
-        if m is None:
-            assert status[n] == 1
-        else:
-            assert status[n] == 0 and np.array_equal(mats[n], m), p
+    _, _, n_tied = _check_search(s, OG.P1, perms, None)
+    assert n_tied >= 1
+    log = []
+    s.solve(tuple(range(7, -1, -1)), None, ties=log)
+    assert log  # the §3.4 reverse-order example has a logged tie
+
+
+@pytest.mark.parametrize("entries", [(-4, -1, 0, 1, 4), (-8, -1, 0, 1, 8)])
+def test_greedy_search_extended_sets(entries):
+    """The extended entry sets of P:L1206-1235 ({0, +-1, +-4}, {0, +-1, +-8}; |D| = 5^8), rows 1
+    and 5 fixed, all 720 orders: matrices, feasibility and ties equal the oracle's."""
+    s = OG.Search(entries)
+    free = [k for k in range(8) if k not in OG.FIXED_ROWS]
+    _check_search(s, entries, list(_it.permutations(free)), OG.FIXED_ROWS)
 
 
 def test_greedy_search_invalid_sequences():
@@ -649,6 +766,27 @@ def test_config3_full_size_sampled(mats):
         x = imgs[f:f + 1].cpu().numpy()
         assert np.array_equal(q[f:f + 1].cpu().numpy(), oracle.quantize(oracle.forward_int(M.T1, x), n, 16))
     del imgs, q
+    torch.cuda.empty_cache()
+
+
+def test_config5_full_size_in_place(mats):
+    """BASELINE config 5 at its largest size, in the launch configuration bench.py times: 2^30
+    int16 blocks (137 GB) resident, fused round trip IN PLACE.  r = 64 with T1 and then with C:
+    the stack still equals the generated blocks (sampled batches re-generated); then r = 10 in
+    place, sampled blocks against the oracle reconstruction of the regenerated originals."""
+    torch.cuda.empty_cache()
+    nb = 1 << 30
+    x = synth.laplace_range(0, nb, seed=5, device=DEV)
+    starts = [0, 12345 * 4096, nb // 2, nb - 4096]
+    for name in ("T1", "DCT"):
+        adct.approx_dct8x8_roundtrip(mats[name], x, 64, torch.int16, recon=x)
+        for a in starts:
+            assert torch.equal(x[a:a + 4096], synth.laplace_range(a, a + 4096, seed=5, device=DEV))
+    adct.approx_dct8x8_roundtrip(mats["T1"], x, 10, torch.int16, recon=x)
+    for a in starts:
+        orig = synth.laplace_range(a, a + 256, seed=5, device=DEV).cpu().numpy()  # the same generator
+        _check_int_recon(x[a:a + 256].cpu().numpy(), _oracle_recon("T1", orig, 10))
+    del x
     torch.cuda.empty_cache()
 
 
