@@ -404,25 +404,33 @@ def run_config(args):
                  {"roundtrip_bit_exact": ok})
             del x, rec
     if args.config in ("SSIM", "all"):
-        # next row f1: fused round trip (fwd -> retain r=14 -> inv, fp32 recon) then SSIM with
-        # 8x8 windows (reading A18) on the 512 luma frames of config 4
+        # next row f1: forward -> retain r=14 -> inverse -> SSIM with 8x8 windows (reading A18) on
+        # 128 luma frames of config 4, in ONE kernel (approx_dct8x8_ssim: no reconstruction in
+        # HBM); the two-call pipeline (fp32 reconstruction written and re-read) is timed beside it
         n = 128
         y = synth.ar1_stack(n, 2160, 3840, 0.95, seed=4, device=dev, batch=8)
         m = adct.Matrix.from_int(catalog.T1, "T1")
         rec = torch.empty(y.shape, dtype=torch.float32, device=dev)
         ws = torch.empty(adct.workspace_bytes(adct.geom_of(y), 1), dtype=torch.uint8, device=dev)
+        out = torch.empty(n, dtype=torch.float64, device=dev)
 
-        def ssim_step():
+        def ssim_pipeline():
             adct.approx_dct8x8_roundtrip(m, y, 14, torch.float32, recon=rec, stream=stream)
             adct.ssim_reduce(y, rec, clip=adct.CLIP, workspace=ws, stream=stream)
 
-        ms, clk = _timed(ssim_step, args.steps, args.warmup, stream, dev)
+        ms_pipe, _ = _timed(ssim_pipeline, args.steps, args.warmup, stream, dev)
+        ms, clk = _timed(lambda: adct.approx_dct8x8_ssim(m, y, 14, clip=adct.CLIP, ssim=out, workspace=ws,
+                                                         stream=stream), args.steps, args.warmup, stream, dev)
         from oracle import ssim as OS
         smp = y[:1, :256, :256].cpu().numpy()
         cpu = cpu_rate(lambda: OS.ssim(smp, smp), 32 * 32)
         cpu["sample"] = "SSIM of one 256x256 crop (oracle windows)"
-        emit(f"SSIM (next row f1): {n} luma frames 3840x2160, T1 round trip r=14 -> fp32 recon -> SSIM 8x8 windows; "
-             "bytes/block = 64 in + 256 recon out + 64 + 256 re-read", "T1", ms, n * 270 * 480, 640, "hbm", clk, cpu)
+        emit(f"SSIM (next row f1): {n} luma frames 3840x2160, T1 round trip r=14 + SSIM 8x8 windows in one kernel "
+             "(approx_dct8x8_ssim; bytes/block = 64 u8 in, + the neighbour strips' shared block column)", "T1", ms,
+             n * 270 * 480, 64, "hbm", clk, cpu,
+             {"pipeline_ms": ms_pipe, "pipeline": "approx_dct8x8_roundtrip (fp32 recon in HBM) + ssim_reduce",
+              "roofline": dict(issue_roofline("SSIM", ms, clk, dev),
+                               note="fp64 window sums + SSIM formula per window (1.06e9 windows per step)")})
         del y, rec
     if args.config in ("C1", "C2", "all"):
         rs = list(range(1, 65))
@@ -471,6 +479,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--planes", action="store_true",
+                    help="one approx_dct8x8_fused_sse_planes call per step (Y+U+V); the roofline event then "
+                         "brackets the three planes")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong (default, BASELINE C4): one 512-frame stack sharded over the GPUs; "
                          "weak: 512 frames per GPU")
@@ -506,25 +517,34 @@ def main():
     n_local = hi - lo
     torch.cuda.synchronize(dev)
     geoms = [adct.geom_of(p) for p in planes]
-    ws = torch.empty(max(adct.workspace_bytes(g, 1) for g in geoms), dtype=torch.uint8, device=dev)
+    ws = torch.empty(max(0 if (not args.planes) else adct.planes_workspace_bytes(geoms),
+                         max(adct.workspace_bytes(g, 1) for g in geoms)), dtype=torch.uint8, device=dev)
     # the global per-frame table (fp64, columns SSE Y/U/V, PSNR Y/U/V): the kernels write this
     # rank's rows directly; each step's buffer is all-reduced on the side stream while the next
     # step runs (every entry has exactly one non-zero contributor: bit-identical to one GPU)
     etab = parallel.ErrorTable(n_total, 6, lo, hi, device=dev, buffers=2)
 
-    # per-step events around the luma launch (the dominant kernel), on the launching stream
+    # per-step events around the dominant kernel, on the launching stream: the luma launch (or with
+    # --planes the approx_dct8x8_fused_sse_planes call of the three planes)
     ev_luma = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
+    outs = [([etab.out(i, b) for i in range(3)], [etab.out(3 + i, b) for i in range(3)]) for b in range(2)]
 
     def step(k, timed=False):
         buf = k % 2
         etab.before_write(buf)
-        for i, p in enumerate(planes):
-            if timed and i == 0:
-                ev_luma[k][0].record(stream)
-            adct.approx_dct8x8_fused_sse(m, p, [R], workspace=ws, sse=etab.out(i, buf), psnr=etab.out(3 + i, buf),
-                                         stream=stream)
-            if timed and i == 0:
+        if timed:
+            ev_luma[k][0].record(stream)
+        if (not args.planes):
+            for i, p in enumerate(planes):
+                adct.approx_dct8x8_fused_sse(m, p, [R], workspace=ws, sse=outs[buf][0][i], psnr=outs[buf][1][i],
+                                             stream=stream)
+                if timed and i == 0:
+                    ev_luma[k][1].record(stream)
+        else:
+            adct.approx_dct8x8_fused_sse_planes(m, planes, R, sse=outs[buf][0], psnr=outs[buf][1], workspace=ws,
+                                                stream=stream)
+            if timed:
                 ev_luma[k][1].record(stream)
         etab.combine(buf, stream=side)
         return buf
@@ -557,10 +577,11 @@ def main():
     value = blocks_total / (ms_step * 1e-3)
     table = etab.table_of(last)
 
-    # dominant kernel: this rank's luma launch (fused_u8_tc_kernel + its finalize_kernel;
-    # n_local x 32,400 blocks x 64 algorithmic bytes), averaged over the timed steps
+    # dominant kernel: this rank's luma launch (fused_u8_tc_kernel + its finalize;
+    # n_local x 32,400 blocks x 64 algorithmic bytes) -- with --planes the Y+U+V call
+    # (n_local x 194,400 blocks) -- averaged over the timed steps
     luma_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_luma)
-    luma_blocks = n_local * (H // 8) * (W // 8)
+    luma_blocks = n_local * ((H // 8) * (W // 8) if (not args.planes) else BLOCKS_PER_FRAME)
     luma_bytes = luma_blocks * 64
     hbm_peak, peak_kind = peaks()
     achieved = luma_bytes / (luma_ms * 1e-3) / 1e9
@@ -569,13 +590,21 @@ def main():
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             nt = json.load(f)["simt" if os.environ.get("ADCT_HOT") == "simt" else "tc"]
             traffic, ipb = nt.get("bytes_per_launch"), nt.get("instructions_per_block")
-            if traffic is not None:  # recorded for the 512-frame luma launch; per launch here
-                traffic = traffic * n_local / FRAMES
+            if traffic is not None:  # recorded per 512-frame launch of what the kernel covers
+                traffic = traffic * n_local / FRAMES if nt.get("covers", "luma") == ("luma" if (not args.planes)
+                                                                                    else "yuv") else None
     except Exception:
         pass
 
-    # per-plane PSNR of the first frame of the stack, from the library (finalize kernel, fp64)
+    # per-plane PSNR of the first frame of the stack, from the library (finalize kernel, fp64);
+    # and, outside the timed region, the same frame under the clip policy of SPEC S:L604 ([0, 255]
+    # before the error, reading A6; the generic fused kernels): both metrics are reported
     row0 = table[0].cpu()
+    clip0 = {}
+    if rank == 0:
+        for name, p in zip("YUV", planes):
+            _, pc = adct.approx_dct8x8_fused_sse(m, p[:1], [R], clip=adct.CLIP, return_psnr=True)
+            clip0[name] = float(pc[0, 0])
 
     # end-to-end through the host-buffer C-ABI call (pinned host frames, H2D + D2H inside)
     e2e = None
@@ -628,7 +657,8 @@ def main():
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": ("fused_u8_wtile_kernel<T1Mat,10> (SIMT)" if os.environ.get("ADCT_HOT") == "simt"
                                     else "fused_u8_tc_kernel<T1Mat,10> (tcgen05 kind::i8)") +
-                                   f" + finalize_kernel (luma plane, {luma_blocks:,} blocks x 64 B)",
+                                   (f" + finalize_kernel (luma plane, {luma_blocks:,} blocks x 64 B)" if (not args.planes)
+                                    else f" x 3 planes + finalizes (Y+U+V call, {luma_blocks:,} blocks x 64 B)"),
                          "kernel_ms": luma_ms},
             # the whole step (Y + U + V + finalizes + the table combine), rank 0's share
             "roofline_step": {"bound": "hbm", "achieved": n_local * BLOCKS_PER_FRAME * 64 / (ms_step * 1e-3) / 1e9,
@@ -647,6 +677,7 @@ def main():
             "cpu_baseline": cpu,
             "sse_frame0": {"Y": float(row0[0]), "U": float(row0[1]), "V": float(row0[2])},
             "psnr_frame0_dB": {"Y": float(row0[3]), "U": float(row0[4]), "V": float(row0[5])},
+            "psnr_frame0_clipped_dB": clip0,
         }
         print(json.dumps(line), flush=True)
     if parallel.env_rank()[2] > 1:

@@ -146,7 +146,10 @@ adct_status psnr_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
  * (reading A20) -> inverse C_hat^T B' C_hat, one pass, written as a reconstruction.
  * n: 16 or 32.  src: device U8/I16 images with geometry g, H and W multiples of n, 16-byte
  * aligned base and strides; recon: same geometry, dtype/clip policy as approx_dct8x8_roundtrip.
- * r in 1..n^2.  The fp32 forward is exact for |samples| <= 7281. */
+ * r in 1..n^2.  Every intermediate of the fp32 forward is an exact integer for |samples| <=
+ * 7281; beyond that (int16 sources) the forward rounds like any fp32 transform: tested over the
+ * whole int16 range to the north star's 1e-5 per-block bound, and the int16 round trip at
+ * r = n^2 stays the identity there (tests/test_gpu_parity.py::test_jam_full_int16_range). */
 adct_status approx_dct_jam_roundtrip(int32_t n, const void* src, adct_dtype src_t, adct_geom g, int32_t r,
                                      void* recon, adct_dtype recon_t, adct_clip clip, void* stream);
 
@@ -202,6 +205,16 @@ adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
 
 /* --- fused performance paths (must equal the composition of the calls above) ----------- */
 
+/* Forward -> retain r -> inverse -> SSIM per image, reading each block once and never writing
+ * the reconstruction (SSIM as the paper's second figure of merit, P:L2258-2283,
+ * P:L2345-2361; reading A18): exactly ssim_reduce(src, ADCT_U8, recon, ADCT_F32, g, 255, clip,
+ * ssim, ...) of recon = approx_dct8x8_roundtrip(m, src, ADCT_U8, g, r, ADCT_F32, ADCT_CLIP_NONE).
+ * src: device u8 images (8-byte aligned rows), H, W >= 8 multiples of 8; any matrix; r in 1..64;
+ * clip: the policy ssim_reduce applies to the reconstruction ([0, 255]).  ssim: device fp64
+ * [n_images].  workspace >= adct_workspace_bytes(g, 1).  Deterministic. */
+adct_status approx_dct8x8_ssim(const adct_matrix* m, const uint8_t* src, adct_geom g, int32_t r, adct_clip clip,
+                               double* ssim, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Forward -> zonal retention (first r in zig-zag order) -> inverse, written as a
  * reconstruction, with each block read once and its coefficients kept in registers: the
  * composition approx_dct8x8_fwd -> zonal_retain -> approx_dct8x8_inv (
@@ -238,6 +251,21 @@ adct_status approx_dct8x8_fused_sse_host(const adct_matrix* m, const void* src_h
                                          const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse_host,
                                          double* psnr_host, int64_t chunk_images, void* workspace,
                                          size_t workspace_bytes, void* stream);
+
+/* Several planes in ONE call -- the Y, U and V planes of a 4:2:0 stack (BASELINE config 4,
+ * per-plane PSNR as in P:L2868): for each plane i exactly approx_dct8x8_fused_sse(m, src[i],
+ * src_t, g[i], &r, 1, clip, sse[i], psnr[i], ...), one r.  n_planes in 1..ADCT_MAX_PLANES; the
+ * planes may differ in geometry (not in n_images semantics: each plane's sse[i] / psnr[i] is a
+ * device fp64 [g[i].n_images]).  psnr may be NULL, or hold NULL entries.  The planes run one
+ * after the other on the stream (u8 planes without clip whose widths are multiples of 128 on the
+ * tensor-core kernel, all of them or none).  workspace >= adct_planes_workspace_bytes(n_planes, g)
+ * (the planes' partials side by side). */
+#define ADCT_MAX_PLANES 3
+size_t adct_planes_workspace_bytes(int32_t n_planes, const adct_geom* g);
+adct_status approx_dct8x8_fused_sse_planes(const adct_matrix* m, int32_t n_planes, const void* const* src,
+                                           adct_dtype src_t, const adct_geom* g, int32_t r, adct_clip clip,
+                                           double* const* sse, double* const* psnr, void* workspace,
+                                           size_t workspace_bytes, void* stream);
 
 /* Forward transform with S folded into a uniform quantiser (BASELINE.json config 3):
  * q_kl = round_half_away(Y_kl / (step * sqrt(n_k n_l)))  (reading A10), int16 block-major.

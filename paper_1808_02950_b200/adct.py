@@ -29,7 +29,8 @@ SYMBOLS = [
     "approx_dct8x8_fused_sse", "adct_host_workspace_bytes", "approx_dct8x8_fused_sse_host",
     "approx_dct8x8_fwd_quant", "adct_workspace_bytes", "adct_status_str", "adct_launch_count",
     "approx_dct8x8_roundtrip", "ssim_reduce", "approx_dct_jam_roundtrip", "adct_greedy_workspace_bytes",
-    "adct_greedy_search", "adct_merit_batch", "adct_matrix_chat",
+    "adct_greedy_search", "adct_merit_batch", "adct_matrix_chat", "adct_planes_workspace_bytes",
+    "approx_dct8x8_fused_sse_planes", "approx_dct8x8_ssim",
 ]
 
 
@@ -62,6 +63,12 @@ def _load() -> ctypes.CDLL:
     L.approx_dct8x8_inv.argtypes = [P, P, S, Geom, P, S, S, P]
     L.psnr_reduce.argtypes = [P, S, P, S, Geom, D, S, P, P, P, ctypes.c_size_t, P]
     L.approx_dct8x8_fused_sse.argtypes = [P, P, S, Geom, P, I32_, S, P, P, P, ctypes.c_size_t, P]
+    if hasattr(L, "adct_planes_workspace_bytes") or not os.environ.get("ADCT_LIB"):  # A/B builds may predate it
+        L.adct_planes_workspace_bytes.argtypes = [I32_, P]
+        L.adct_planes_workspace_bytes.restype = ctypes.c_size_t
+        L.approx_dct8x8_fused_sse_planes.argtypes = [P, I32_, P, S, P, I32_, S, P, P, P, ctypes.c_size_t, P]
+    if hasattr(L, "approx_dct8x8_ssim") or not os.environ.get("ADCT_LIB"):
+        L.approx_dct8x8_ssim.argtypes = [P, P, Geom, I32_, S, P, P, ctypes.c_size_t, P]
     L.adct_host_workspace_bytes.argtypes = [Geom, I32_, I64_, S]
     L.adct_host_workspace_bytes.restype = ctypes.c_size_t
     L.approx_dct8x8_fused_sse_host.argtypes = [P, P, S, Geom, P, I32_, S, P, P, I64_, P, ctypes.c_size_t, P]
@@ -81,8 +88,11 @@ def _load() -> ctypes.CDLL:
     L.adct_launch_count.argtypes = []
     L.adct_launch_count.restype = I64_
     for name in SYMBOLS:
+        if os.environ.get("ADCT_LIB") and not hasattr(L, name):
+            continue
         fn = getattr(L, name)
         if name not in ("adct_matrix_destroy", "adct_host_workspace_bytes", "adct_workspace_bytes",
+                        "adct_planes_workspace_bytes",
                         "adct_status_str", "adct_launch_count", "adct_greedy_workspace_bytes"):
             fn.restype = S
     return L
@@ -404,6 +414,49 @@ def approx_dct8x8_fused_sse(m: Matrix, src: torch.Tensor, r_list, clip: int = CL
     return (sse, psnr) if want_psnr else sse
 
 
+MAX_PLANES = 3
+
+
+def planes_workspace_bytes(geoms) -> int:
+    arr = (Geom * len(geoms))(*geoms)
+    return int(lib.adct_planes_workspace_bytes(len(geoms), ctypes.cast(arr, ctypes.c_void_p)))
+
+
+def approx_dct8x8_fused_sse_planes(m: Matrix, planes, r: int, clip: int = CLIP_NONE, sse=None, psnr=None,
+                                   workspace: torch.Tensor | None = None, stream=None):
+    """The planes of one stack (e.g. Y, U, V) in one call: per plane SSE and PSNR [n] (fp64, device).
+    `sse` / `psnr`: optional lists of output tensors (a psnr entry may be None).  Returns (sse, psnr)."""
+    n = len(planes)
+    if not 1 <= n <= MAX_PLANES:
+        raise ValueError(f"1..{MAX_PLANES} planes")
+    geoms = [geom_of(p) for p in planes]
+    dt = dtype_code(planes[0])
+    if any(dtype_code(p) != dt or p.device != planes[0].device for p in planes):
+        raise ValueError("planes must share dtype and device")
+    dev = planes[0].device
+    if sse is None:
+        sse = [torch.empty(g.n_images, dtype=torch.float64, device=dev) for g in geoms]
+    if psnr is None:
+        psnr = [torch.empty(g.n_images, dtype=torch.float64, device=dev) for g in geoms]
+    for i, g in enumerate(geoms):
+        _out(sse[i], g.n_images, planes[i], "sse", dtype=torch.float64)
+        if psnr[i] is not None:
+            _out(psnr[i], g.n_images, planes[i], "psnr", dtype=torch.float64)
+    nbytes = planes_workspace_bytes(geoms)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    P = ctypes.c_void_p
+    srcs = (P * n)(*[p.data_ptr() for p in planes])
+    garr = (Geom * n)(*geoms)
+    sarr = (P * n)(*[t.data_ptr() for t in sse])
+    parr = (P * n)(*[(t.data_ptr() if t is not None else None) for t in psnr])
+    _check(lib.approx_dct8x8_fused_sse_planes(m.handle, n, ctypes.cast(srcs, P), dt, ctypes.cast(garr, P), int(r),
+                                              int(clip), ctypes.cast(sarr, P), ctypes.cast(parr, P),
+                                              workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)),
+           "approx_dct8x8_fused_sse_planes")
+    return sse, psnr
+
+
 def host_workspace_bytes(geom: Geom, n_r: int, chunk_images: int, src_dtype: int = U8) -> int:
     return int(lib.adct_host_workspace_bytes(geom, n_r, chunk_images, src_dtype))
 
@@ -430,6 +483,22 @@ def approx_dct8x8_fused_sse_host(m: Matrix, src_host: torch.Tensor, r_list, work
                                             int(chunk_images), workspace.data_ptr(), workspace.numel(),
                                             _stream_ptr(stream)), "approx_dct8x8_fused_sse_host")
     return (sse_host, psnr_host) if want_psnr else sse_host
+
+
+def approx_dct8x8_ssim(m: Matrix, src: torch.Tensor, r: int, clip: int = CLIP, ssim: torch.Tensor | None = None,
+                       workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Forward -> retain r -> inverse -> SSIM per image (fp64 [n], device) in one pass over the u8
+    images; equals ssim_reduce(src, approx_dct8x8_roundtrip(m, src, r, float32), clip=clip)."""
+    g = geom_of(src)
+    if ssim is None:
+        ssim = torch.empty(g.n_images, dtype=torch.float64, device=src.device)
+    _out(ssim, g.n_images, src, "ssim", dtype=torch.float64)
+    nbytes = workspace_bytes(g, 1)
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=src.device)
+    _check(lib.approx_dct8x8_ssim(m.handle, src.data_ptr(), g, int(r), int(clip), ssim.data_ptr(),
+                                  workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)), "approx_dct8x8_ssim")
+    return ssim
 
 
 def approx_dct8x8_fwd_quant(m: Matrix, src: torch.Tensor, step: int = 16, q: torch.Tensor | None = None,

@@ -184,6 +184,11 @@ constexpr int kTcDStages = kTcWays;               // TMEM accumulator stages (N 
 #define ADCT_TC_CHUNK 24
 #endif
 constexpr int kTcChunkTiles = ADCT_TC_CHUNK;      // tiles per chunk
+constexpr int kTcMaxPlanes = 3;                   // planes per approx_dct8x8_fused_sse_planes call (Y, U, V)
+#ifndef ADCT_TC_ABL
+#define ADCT_TC_ABL 0  // ablation builds only (tools/build_variant.sh): 1 no epilogue math, 2 no TMEM load, 3 no MMA
+#endif
+
 constexpr int kTcPartials = 4 * kTcEpi;           // partials per chunk
 constexpr int kTcBBytes = 160 * 128;              // B: N <= 160 outputs x K = 128 s8
 constexpr int kTcBars = 2 * kTcSlots + 4 * kTcDStages;

@@ -435,11 +435,116 @@ __global__ void __launch_bounds__(kSsNT) ssim_strip_kernel(const OrigT* __restri
   if (lane == 0) partial[(int64_t)img * units + q] = acc;
 }
 
+// ---- fused round trip + SSIM (next row f1 "in the fused epilogue"): no reconstruction in HBM --
+// One warp per (image, strip of 24 window columns = 32 pixel columns = 4 block columns, block
+// aligned); the warp walks the whole image height in chunks of 8 block rows.  Per chunk, lane l
+// reconstructs block (row 8c + l/4, column 3s + l%4) exactly as roundtrip_kernel does (fwd2d,
+// weights wk, inv2d) and writes it (fp32 reconstruction, u8 original) into the warp's shared
+// 72-row window (rows 0..7 carry the previous chunk's last 8 rows); then lane l takes pixel
+// column 24s + l through those 64 rows with ss_group -- the strip kernel's vertical running sums,
+// shuffle window sums and SSIM formula (lanes 0..23 own windows).  The running sums continue
+// across chunks: they add and subtract exactly representable fp64 values (u8 sums in fp32), so
+// they never drift.  HBM traffic: the u8 original once, + 1/3 re-read of the neighbour strips'
+// shared block column (mostly from L2); nothing is written but one fp64 partial per warp.
+constexpr int kSfOut = 24, kSfWarps = 3, kSfPitch = 36, kSfRows = 72;  // 38 KB static smem
+
+template <class MP, int CLIP>
+__global__ void __launch_bounds__(32 * kSfWarps) ssim_fused_kernel(const uint8_t* __restrict__ src, KGeom g,
+                                                                   int32_t height, int32_t width, DevMat dm, Wk wk,
+                                                                   int32_t nstrips, int64_t total_units, float lo,
+                                                                   float hi, double c1s, double c2s,
+                                                                   double* __restrict__ partial) {
+  __shared__ __align__(16) float sy[kSfWarps][kSfRows][kSfPitch];
+  __shared__ __align__(16) uint8_t sx[kSfWarps][kSfRows][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * kSfWarps + w;
+  if (u >= total_units) return;  // warp-uniform; the warps never synchronise with each other
+  const int32_t img = (int32_t)(u / nstrips), strip = (int32_t)(u - (int64_t)img * nstrips);
+  const int32_t nbh = height / 8, nbw = width / 8;
+  const int32_t bx = 3 * strip + (lane & 3), brl = lane >> 2;  // this lane's block (column, row in chunk)
+  const int32_t xcol = 24 * strip + lane;                      // this lane's pixel column (SSIM phase)
+  const bool win_ok = lane < kSfOut && xcol <= width - 8;
+  const MP m(dm);
+  const uint8_t* base = src + (int64_t)img * g.image_stride + (int64_t)bx * 8;
+  float(*Y)[kSfPitch] = sy[w];
+  uint8_t(*X)[32] = sx[w];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {  // the rows above the image: zero
+    Y[i][lane] = 0.0f;
+    X[i][lane] = 0;
+  }
+  // this lane's block of chunk 0, raw
+  uint2 raw[8];
+  auto load_raw = [&](int32_t c) {
+    const int32_t by = 8 * c + brl;
+    const bool ok = by < nbh && bx < nbw;
+    const uint8_t* p = base + (int64_t)by * 8 * g.row_stride;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) raw[i] = ok ? Src<uint8_t>::load(p + (int64_t)i * g.row_stride) : make_uint2(0u, 0u);
+  };
+  load_raw(0);
+  SsState<float> st{0.0f, 0.0f, 0.0, 0.0, 0.0, 0.0};
+  const int32_t nchunks = (height + 63) / 64;
+  for (int32_t c = 0; c < nchunks; ++c) {
+    {  // round trip of the lane's block (the composition approx_dct8x8_roundtrip, F32, no clip)
+      float x[8][8], y[8][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) Src<uint8_t>::to_f(raw[i], x[i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<uint2*>(&X[8 + 8 * brl + i][8 * (lane & 3)]) = raw[i];
+      fwd2d(m, x, y);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) y[k][l] *= wk.w[k * 8 + l];
+      inv2d<MP, ~0ull>(m, y, x);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float* d = &Y[8 + 8 * brl + i][8 * (lane & 3)];
+        *reinterpret_cast<float4*>(d) = make_float4(x[i][0], x[i][1], x[i][2], x[i][3]);
+        *reinterpret_cast<float4*>(d + 4) = make_float4(x[i][4], x[i][5], x[i][6], x[i][7]);
+      }
+    }
+    if (c + 1 < nchunks) load_raw(c + 1);  // the next chunk's block lands during the SSIM phase
+    __syncwarp();
+    // SSIM phase: groups of 8 rows gi = 8c + q (global rows 64c + 8q ..), dropping the group 8 rows up
+#pragma unroll 1
+    for (int q = 0; q < 8; ++q) {
+      SsGroup<uint8_t, float> cur, prev;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        cur.a[k] = X[8 + 8 * q + k][lane];
+        cur.b[k] = Y[8 + 8 * q + k][lane];
+        prev.a[k] = X[8 * q + k][lane];
+        prev.b[k] = Y[8 * q + k][lane];
+      }
+      ss_group<CLIP>(st, cur, prev, 8 * c + q, height - 7, win_ok, lo, hi, c1s, c2s);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // carry the chunk's last 8 rows
+      Y[i][lane] = Y[64 + i][lane];
+      X[i][lane] = X[64 + i][lane];
+    }
+    __syncwarp();
+  }
+  double acc = st.acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) partial[u] = acc;
+}
+
 }  // namespace
 
 int64_t ssim_tiles(const adct_geom& g) {  // warps (strip x band units) per image
   if (g.height < 8 || g.width < 8) return 0;
   return (int64_t)((g.width - 7 + kSsOut - 1) / kSsOut) * ((g.height - 7 + kSsTY - 1) / kSsTY);
+}
+
+int64_t ssim_fused_strips(const adct_geom& g) {  // warps of ssim_fused_kernel per image
+  if (g.height < 8 || g.width < 8) return 0;
+  return (int64_t)((g.width - 7 + kSfOut - 1) / kSfOut);
 }
 
 void launch_finalize_scaled(const double* partial, int32_t chunks, int64_t n_images, double scale, double* out,
@@ -670,6 +775,44 @@ adct_status ssim_reduce(const void* orig, adct_dtype orig_t, const void* recon, 
   if (adct_status e = launch_status()) return e;
   const double nwin = (double)(g.height - 7) * (double)(g.width - 7);
   launch_finalize_scaled(partial, units, g.n_images, 1.0 / nwin, ssim, st);
+  return launch_status();
+}
+
+adct_status approx_dct8x8_ssim(const adct_matrix* m, const uint8_t* src, adct_geom g, int32_t r, adct_clip clip,
+                               double* ssim, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!m || !src || !ssim) return ADCT_E_INVALID_ARGUMENT;
+  if (adct_status s = check_geom(g)) return s;
+  if (r < 1 || r > 64) return ADCT_E_INVALID_ARGUMENT;
+  if (clip != ADCT_CLIP_NONE && clip != ADCT_CLIP && clip != ADCT_CLIP_ROUND) return ADCT_E_INVALID_ARGUMENT;
+  if (!aligned(src, 8)) return ADCT_E_ALIGNMENT;
+  if (!workspace || workspace_bytes < adct_workspace_bytes(g, 1) || !aligned(workspace, 8)) return ADCT_E_WORKSPACE;
+  if (g.n_images == 0) return ADCT_OK;
+  const KGeom kg = make_kgeom(g);
+  Wk wk;
+  const uint64_t keep = keep_mask(r);
+  for (int p = 0; p < 64; ++p) wk.w[p] = ((keep >> p) & 1ull) ? (m->is_int ? m->dev.wy[p] : m->dev.wb[p]) : 0.0f;
+  const int32_t nstrips = (int32_t)ssim_fused_strips(g);
+  const int64_t total = (int64_t)nstrips * g.n_images;
+  const double peak = 255.0, c1 = (0.01 * peak) * (0.01 * peak), c2 = (0.03 * peak) * (0.03 * peak);
+  const unsigned grid = (unsigned)((total + kSfWarps - 1) / kSfWarps);
+  double* partial = (double*)workspace;
+  cudaStream_t st = (cudaStream_t)stream;
+#define ADCT_SF(MP, C)                                                                                        \
+  ssim_fused_kernel<MP, C><<<grid, 32 * kSfWarps, 0, st>>>(src, kg, g.height, g.width, m->dev, wk, nstrips, total, \
+                                                           0.0f, (float)peak, 4096.0 * c1, 4096.0 * c2, partial)
+#define ADCT_SF_M(MP)                                         \
+  do {                                                        \
+    if (clip == ADCT_CLIP_NONE) ADCT_SF(MP, ADCT_CLIP_NONE);  \
+    else if (clip == ADCT_CLIP) ADCT_SF(MP, ADCT_CLIP);       \
+    else ADCT_SF(MP, ADCT_CLIP_ROUND);                        \
+  } while (0)
+  if (m->specialized) ADCT_SF_M(T1Mat); else ADCT_SF_M(RtMat);
+#undef ADCT_SF_M
+#undef ADCT_SF
+  count_launch();
+  if (adct_status e = launch_status()) return e;
+  const double nwin = (double)(g.height - 7) * (double)(g.width - 7);
+  launch_finalize_scaled(partial, nstrips, g.n_images, 1.0 / nwin, ssim, st);
   return launch_status();
 }
 

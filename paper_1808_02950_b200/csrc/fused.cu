@@ -26,6 +26,10 @@ bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g,
                    cudaStream_t st, adct_status* status);
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
                      double* partial, cudaStream_t st, adct_status* status);
+bool fused_u8_tc_planes(const adct_matrix* m, int n, const uint8_t* const* src, const adct_geom* g, int32_t r,
+                        double* const* sse, double* const* psnr, double* const* partial, cudaStream_t st,
+                        adct_status* status);
+bool tc_hot_enabled();
 
 namespace {
 
@@ -351,6 +355,62 @@ adct_status approx_dct8x8_fused_sse_host(const adct_matrix* m, const void* src_h
   return st;
 }
 
+size_t adct_planes_workspace_bytes(int32_t n_planes, const adct_geom* g) {
+  if (n_planes < 1 || n_planes > ADCT_MAX_PLANES || !g) return 0;
+  size_t tot = 0;
+  for (int i = 0; i < n_planes; ++i) tot += (adct_workspace_bytes(g[i], 1) + 255) / 256 * 256;
+  return tot;
+}
+
+adct_status approx_dct8x8_fused_sse_planes(const adct_matrix* m, int32_t n_planes, const void* const* src,
+                                           adct_dtype src_t, const adct_geom* g, int32_t r, adct_clip clip,
+                                           double* const* sse, double* const* psnr, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  if (!m || !src || !g || !sse || n_planes < 1 || n_planes > ADCT_MAX_PLANES) return ADCT_E_INVALID_ARGUMENT;
+  for (int i = 0; i < n_planes; ++i) {
+    if (g[i].n_images == 0) {  // an empty plane: geometry checked, its buffers may be NULL
+      if (adct_status s = check_geom(g[i])) return s;
+      continue;
+    }
+    if (adct_status s = fused_check(m, src[i], src_t, g[i], &r, 1, clip)) return s;
+    if (!sse[i]) return ADCT_E_INVALID_ARGUMENT;
+  }
+  if (!workspace || workspace_bytes < adct_planes_workspace_bytes(n_planes, g) || !aligned(workspace, 8))
+    return ADCT_E_WORKSPACE;
+  double* part[ADCT_MAX_PLANES];
+  size_t off = 0;
+  for (int i = 0; i < n_planes; ++i) {
+    part[i] = (double*)((char*)workspace + off);
+    off += (adct_workspace_bytes(g[i], 1) + 255) / 256 * 256;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // the tensor-core kernel for every non-empty plane when all of them qualify
+  if (src_t == ADCT_U8 && clip == ADCT_CLIP_NONE && m->is_int && !g_disable_stream && tc_hot_enabled() &&
+      n_planes <= kTcMaxPlanes) {
+    const uint8_t* s8[kTcMaxPlanes];
+    adct_geom gg[kTcMaxPlanes];
+    double *ss[kTcMaxPlanes], *pp[kTcMaxPlanes], *pt[kTcMaxPlanes];
+    int n = 0;
+    for (int i = 0; i < n_planes; ++i) {
+      if (g[i].n_images == 0) continue;
+      s8[n] = (const uint8_t*)src[i];
+      gg[n] = g[i];
+      ss[n] = sse[i];
+      pp[n] = psnr ? psnr[i] : nullptr;
+      pt[n] = part[i];
+      ++n;
+    }
+    if (n == 0) return ADCT_OK;
+    adct_status stt = ADCT_OK;
+    if (fused_u8_tc_planes(m, n, s8, gg, r, ss, pp, pt, st, &stt)) return stt;
+  }
+  for (int i = 0; i < n_planes; ++i)  // the per-plane composition
+    if (g[i].n_images > 0)
+      if (adct_status s = fused_run(m, src[i], src_t, g[i], &r, 1, clip, sse[i], psnr ? psnr[i] : nullptr, part[i], st))
+      return s;
+  return ADCT_OK;
+}
+
 adct_status approx_dct8x8_fwd_quant(const adct_matrix* m, const uint8_t* src, adct_geom g, int32_t step, int16_t* q,
                                     void* stream) {
   if (!m || !src || !q) return ADCT_E_INVALID_ARGUMENT;
@@ -387,3 +447,4 @@ adct_status approx_dct8x8_fwd_quant(const adct_matrix* m, const uint8_t* src, ad
 }
 
 }  // extern "C"
+static_assert(ADCT_MAX_PLANES == adct::kTcMaxPlanes, "plane count of the C-ABI and the kernel");

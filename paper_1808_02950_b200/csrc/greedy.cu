@@ -145,12 +145,14 @@ __global__ void __launch_bounds__(kGrNT) search_kernel(const int8_t* __restrict_
         if (p < np) orth &= (__dp4a((int)w.x, (int)pr[p].x, __dp4a((int)w.y, (int)pr[p].y, 0)) == 0);
       if (!orth) continue;
       const double s = sk[i];
-      if (s > bs) {  // strided scan visits i in increasing order: the first maximum is kept
-        bs = s;
-        bi = i;
-        bn = 1;
-      } else if (s == bs) {
-        ++bn;
+      if (s >= bs) {  // one compare on the common path (s < bs); ties are rare
+        if (s > bs) {   // strided scan visits i in increasing order: the first maximum is kept
+          bs = s;
+          bi = i;
+          bn = 1;
+        } else {
+          ++bn;
+        }
       }
     }
     // CTA argmax of (score, -index): a total order, so the reduction order does not matter

@@ -17,6 +17,7 @@ std::atomic<int64_t> g_launches{0};
 
 int64_t sweep_chunks(const adct_geom& g);
 int64_t ssim_tiles(const adct_geom& g);
+int64_t ssim_fused_strips(const adct_geom& g);
 
 
 namespace {
@@ -279,7 +280,8 @@ size_t adct_workspace_bytes(adct_geom g, int32_t n_r) {
   (void)n_r;  // per-image partials hold all 64 r slots of the sweep kernel
   const int64_t a = (fused_chunks(g) > sweep_chunks(g) ? fused_chunks(g) : sweep_chunks(g)) * 64;
   const int64_t b = sse_chunks(g);
-  const int64_t c = stream_partials_per_image(g) > ssim_tiles(g) ? stream_partials_per_image(g) : ssim_tiles(g);
+  int64_t c = stream_partials_per_image(g) > ssim_tiles(g) ? stream_partials_per_image(g) : ssim_tiles(g);
+  if (ssim_fused_strips(g) > c) c = ssim_fused_strips(g);
   int64_t per = a > b ? a : b;
   if (c > per) per = c;
   return (size_t)(g.n_images > 0 ? g.n_images : 0) * (size_t)per * sizeof(double) + 256;

@@ -415,6 +415,8 @@ static const bool g_hot_simt = [] {
   return e && std::strcmp(e, "simt") == 0;
 }();
 
+bool tc_hot_enabled() { return !g_hot_simt; }
+
 bool fused_u8_stream(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
                      double* partial, cudaStream_t st, adct_status* status) {
   if (!g_hot_simt && fused_u8_tc(m, src, g, r, sse, psnr, partial, st, status)) return true;

@@ -307,6 +307,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           if (tt >= (uint32_t)kTcDStages) mbar_wait_sleep(&dfree[hs], dpar);  // tile tt - D's half h read
           tc_fence_after();
           if (elect_one()) {
+#if ADCT_TC_ABL >= 3  // ablation build: no MMA, the ring only (pure TMA stream rate)
+            mbar_arrive(&dfull[hs]);
+            if (h == 1) mbar_arrive(&sfree[slot]);
+#else
             const uint32_t td = tbase + (uint32_t)NB * hs;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
@@ -314,6 +318,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         kk > 0 ? 1u : 0u);
             mma_commit(smem_u32(&dfull[hs]));                // half h of tile tt written
             if (h == 1) mma_commit(smem_u32(&sfree[slot]));  // the slot may be refilled
+#endif
           }
           __syncwarp();
         }
@@ -345,6 +350,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tc_fence_after();
           const uint32_t tD = tbase + lane_q + (uint32_t)(NB * hs);
           uint32_t yr[S::NY], st[64];
+#if ADCT_TC_ABL >= 2  // ablation build: no TMEM load and no epilogue arithmetic
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dfree[hs]);
+          acc += (float)tD;
+          continue;
+#endif
           if constexpr (S::NY == 16) tmem_ld16(tD, yr);
           else tmem_ld32(tD, yr);
           if constexpr (!S::RESID) {
@@ -356,6 +367,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&dfree[hs]);  // the MMA of tile tt + D may overwrite the half-stage
+#if ADCT_TC_ABL >= 1  // ablation build: TMEM load, no epilogue arithmetic
+          acc += i2f(yr[0]) + i2f(st[0]);
+          continue;
+#endif
           acc += tc_block_sse<MP, R>(m, yr, st);
         }
       }
@@ -373,21 +388,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 template <class MP, int R, int CW>
 bool launch_tc_rc(const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return false;
   // the shared-memory opt-in is a per-device function attribute: set it once per device
   static std::mutex mu;
-  static bool done[64] = {};
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    if (dev < 0 || dev >= 64) return false;
-    if (!done[dev]) {
-      if (cudaFuncSetAttribute(fused_u8_tc_kernel<MP, R, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kTcSmem) != cudaSuccess)
-        return false;
-      done[dev] = true;
-    }
-  }
+  static int8_t state[kMaxDevices] = {};
+  if (!once_per_device(mu, state, [] {
+        return cudaFuncSetAttribute(fused_u8_tc_kernel<MP, R, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kTcSmem) == cudaSuccess;
+      }))
+    return false;
   const int64_t grid = (int64_t)a.n_chunks < sms_s() ? (int64_t)a.n_chunks : sms_s();
   fused_u8_tc_kernel<MP, R, CW><<<(unsigned)grid, kTcThreads, kTcSmem, st>>>(map, a, dm, partial);
   return true;
@@ -445,7 +453,12 @@ TcPlan tc_plan(const adct_geom& g) {
   if (g.width <= 0 || g.height <= 0 || (g.width % 128) != 0) return p;  // whole 128-byte chunks only
   const int64_t nch = g.width / 128, nbd = g.height / 8;
   int64_t best = -1;
+  static const int force_cw = [] {  // A/B hook: ADCT_TC_CW=1|2|16 forces the tile shape
+    const char* e = std::getenv("ADCT_TC_CW");
+    return e ? std::atoi(e) : 0;
+  }();
   for (int cw : {2, 16, 1}) {
+    if (force_cw && cw != force_cw) continue;
     const int64_t bh = 16 / cw;
     const int64_t tiles = ((nch + cw - 1) / cw) * ((nbd + bh - 1) / bh);
     if (best < 0 || tiles < best) {
@@ -488,6 +501,32 @@ bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, i
   launch_finalize(partial, p.cpi * kTcPartials, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0, sse, psnr,
                   st);
   *status = launch_status();
+  return true;
+}
+
+// Several planes (the Y, U, V planes of config 4) on the tensor-core path: all of them or none
+// (false, nothing launched), one launch per plane on the stream.  A single launch over the
+// concatenated chunk lists of the planes (runtime tile shape, plane table) was built and measured:
+// it removed two ramps and tails but its epilogue compiled to a different schedule that ran the
+// luma plane 3-10 % slower and under the power cap (1.49-1.50 ms vs 1.46 ms per C4 step, same box;
+// DESIGN.md §5.2), so the planes run one after the other.
+bool fused_u8_tc_planes(const adct_matrix* m, int n, const uint8_t* const* src, const adct_geom* g, int32_t r,
+                        double* const* sse, double* const* psnr, double* const* partial, cudaStream_t st,
+                        adct_status* status) {
+  if (n < 1 || n > kTcMaxPlanes || !m->is_int) return false;
+  const bool r_ok = m->specialized ? (r == 3 || r == 10 || r == 14) : r == 10;
+  if (!r_ok) return false;
+  for (int i = 0; i < n; ++i) {
+    const TcPlan p = tc_plan(g[i]);
+    if (!p.ok || g[i].n_images == 0 || !aligned(src[i], 16)) return false;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (!fused_u8_tc(m, src[i], g[i], r, sse[i], psnr ? psnr[i] : nullptr, partial[i], st, status)) {
+      *status = ADCT_E_CUDA;  // a plane that passed the checks failed to launch
+      return true;
+    }
+    if (*status != ADCT_OK) return true;
+  }
   return true;
 }
 

@@ -588,6 +588,47 @@ def test_ssim_identical_is_one_and_pipeline(mats):
             assert np.allclose(got, ref, rtol=1e-6), (name, r, got, ref)
 
 
+@pytest.mark.parametrize("shape", [(1, 8, 8), (2, 40, 56), (1, 72, 104), (3, 136, 264), (2, 64, 200), (1, 520, 328)])
+@pytest.mark.parametrize("name", ["T1", "DCT", "T6"])
+def test_ssim_fused_equals_composition(mats, shape, name):
+    """approx_dct8x8_ssim (round trip + SSIM in one kernel, no reconstruction in HBM) equals the
+    composition approx_dct8x8_roundtrip (fp32) -> ssim_reduce for every clip policy: the same fp32
+    reconstruction and exactly representable window sums, only the final per-image summation
+    order differs (1e-12).  Shapes: one window, ragged strips (W - 7 not a multiple of 24), chunks
+    of 64 rows cut by the image bottom, several images."""
+    n, h, w = shape
+    img = images("ar1", n, h, w, seed=h * 7 + w).to(DEV)
+    for r in (3, 14):
+        rec = adct.approx_dct8x8_roundtrip(mats[name], img, r, torch.float32)
+        for clip in (adct.CLIP_NONE, adct.CLIP, adct.CLIP_ROUND):
+            want = adct.ssim_reduce(img, rec, clip=clip).cpu().numpy()
+            got = adct.approx_dct8x8_ssim(mats[name], img, r, clip=clip).cpu().numpy()
+            assert np.allclose(got, want, rtol=1e-12, atol=1e-15), (r, clip, got, want)
+
+
+def test_ssim_fused_against_oracle(mats):
+    """End to end against the oracle (its fp64 reconstruction, A18 SSIM): the fp32 reconstruction
+    bounds the agreement at 1e-6 (as for the two-call pipeline); paper r = 3, 14, and a 520 x 1032 frame."""
+    img = synth.ar1_field(2, 136, 264, 0.95, seed=3)
+    for name in ("T1", "DCT"):
+        for r in (3, 14):
+            got = adct.approx_dct8x8_ssim(mats[name], img.to(DEV), r, clip=adct.CLIP).cpu().numpy()
+            ref = OS.ssim(img.numpy(), _oracle_recon(name, img.numpy(), r), clip=1)
+            assert np.allclose(got, ref, rtol=1e-6), (name, r, got, ref)
+    y = synth.ar1_field(1, 520, 1032, 0.95, seed=4)  # many strips and chunks (the 4K oracle takes 26 s)
+    got = adct.approx_dct8x8_ssim(mats["T1"], y.to(DEV), 14, clip=adct.CLIP).cpu().numpy()
+    ref = OS.ssim(y.numpy(), _oracle_recon("T1", y.numpy(), 14), clip=1)
+    assert np.allclose(got, ref, rtol=1e-6)
+
+
+def test_ssim_fused_argument_errors(mats):
+    x = torch.zeros((1, 16, 16), dtype=torch.uint8, device=DEV)
+    for bad_r in (0, 65):
+        with pytest.raises(adct.AdctError):
+            adct.approx_dct8x8_ssim(mats["T1"], x, bad_r)
+    assert float(adct.approx_dct8x8_ssim(mats["T1"], x, 64)[0]) == pytest.approx(1.0, abs=1e-12)  # r = 64: x itself
+
+
 # --- 16/32-point JAM transforms (next row f2; readings A19, A20) ---------------------------------
 
 from oracle import jam as OJ  # noqa: E402

@@ -139,3 +139,39 @@ def test_kernel_variants_agree_with_oracle(tmp_path, env):
         img = synth.ar1_field(n, h, w, 0.95, seed=h + w)
         ref.append(oracle.codec_sse(img.numpy(), [10], t=M.T1).ravel())
     _check(got, np.concatenate(ref))
+
+
+# --- several planes in one launch (approx_dct8x8_fused_sse_planes; the Y, U, V planes of C4) ------
+
+@pytest.mark.parametrize("shapes", [
+    [(3, 2160, 3840), (3, 1080, 1920), (3, 1080, 1920)],   # C4 frames: Y + U + V, one launch
+    [(2, 136, 384), (5, 72, 256)],                          # planes with different image counts
+    [(1, 64, 128), (0, 64, 128), (2, 40, 1280)],            # an empty plane, ragged bands
+    [(2, 64, 200), (2, 64, 256)],                           # width % 128 != 0: per-plane fallback
+])
+def test_planes_equal_per_plane_calls(mats, shapes):
+    """The planes call equals the per-plane approx_dct8x8_fused_sse bit for bit (SSE and PSNR) and
+    the oracle; per-image sums do not depend on which planes share the launch."""
+    planes = [synth.ar1_field(n, h, w, 0.95, seed=100 + i) if n else torch.empty((0, h, w), dtype=torch.uint8)
+              for i, (n, h, w) in enumerate(shapes)]
+    dp = [p.to(DEV) for p in planes]
+    sse, psnr = adct.approx_dct8x8_fused_sse_planes(mats["T1"], dp, 10)
+    for p, d, s, q in zip(planes, dp, sse, psnr):
+        if p.shape[0] == 0:
+            assert s.numel() == 0
+            continue
+        s1, q1 = adct.approx_dct8x8_fused_sse(mats["T1"], d, [10], return_psnr=True)
+        assert torch.equal(s, s1[:, 0]) and torch.equal(q, q1[:, 0])
+        if p.shape[1] * p.shape[2] <= 1080 * 1920:
+            ref = oracle.codec_sse(p.numpy(), [10], t=M.T1)[:, 0]
+            assert np.all(np.abs(s.cpu().numpy() - ref) <= 1e-5 * ref)
+
+
+def test_planes_argument_errors(mats):
+    y = torch.zeros((1, 64, 128), dtype=torch.uint8, device=DEV)
+    with pytest.raises(ValueError):
+        adct.approx_dct8x8_fused_sse_planes(mats["T1"], [y] * 4, 10)
+    with pytest.raises(adct.AdctError):
+        adct.approx_dct8x8_fused_sse_planes(mats["T1"], [y], 0)
+    with pytest.raises(ValueError):
+        adct.approx_dct8x8_fused_sse_planes(mats["T1"], [y, y.to(torch.int16)], 10)

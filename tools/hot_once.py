@@ -35,5 +35,5 @@ nb = frames * 270 * 480
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 gbs = nb * 64 / ms / 1e6
-print(json.dumps({"hot": os.environ.get("ADCT_HOT", "simt"), "frames": frames, "ms": ms, "gblocks_s": nb / ms / 1e6,
+print(json.dumps({"hot": os.environ.get("ADCT_HOT", "tc"), "frames": frames, "ms": ms, "gblocks_s": nb / ms / 1e6,
                   "gbs": gbs, "frac": gbs / peak, "sse0": float(out[0, 0])}))

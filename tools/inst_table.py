@@ -15,6 +15,7 @@ import sys
 CASES = {  # name: (csv, kernel regex, grids or None, executions of the timed function)
     "C2": ("inst_C2.csv", r"fused_sweep_kernel|finalize_kernel", None, 4),
     "MERIT": ("inst_MERIT.csv", r"merit_kernel", None, 5),
+    "SSIM": ("inst_SSIM.csv", r"ssim_fused_kernel", None, 4),
     "GREEDY D2": ("inst_GREEDY.csv", r"digits_kernel|score_kernel|search_kernel", {"(1526, 1, 1)", "(720, 1, 1)"}, 5),
     "GREEDY D1": ("inst_GREEDY.csv", r"digits_kernel|score_kernel|search_kernel", {"(26, 1, 1)", "(40320, 1, 1)"}, 5),
 }
