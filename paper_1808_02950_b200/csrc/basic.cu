@@ -448,8 +448,11 @@ __global__ void __launch_bounds__(kSsNT) ssim_strip_kernel(const OrigT* __restri
 // shared block column (mostly from L2); nothing is written but one fp64 partial per warp.
 constexpr int kSfOut = 24, kSfWarps = 3, kSfPitch = 36, kSfRows = 72;  // 38 KB static smem
 
+#ifndef ADCT_SF_MINB
+#define ADCT_SF_MINB 1
+#endif
 template <class MP, int CLIP>
-__global__ void __launch_bounds__(32 * kSfWarps) ssim_fused_kernel(const uint8_t* __restrict__ src, KGeom g,
+__global__ void __launch_bounds__(32 * kSfWarps, ADCT_SF_MINB) ssim_fused_kernel(const uint8_t* __restrict__ src, KGeom g,
                                                                    int32_t height, int32_t width, DevMat dm, Wk wk,
                                                                    int32_t nstrips, int64_t total_units, float lo,
                                                                    float hi, double c1s, double c2s,
