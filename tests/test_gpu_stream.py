@@ -118,15 +118,19 @@ _VARIANT_SCRIPT = textwrap.dedent("""
     from paper_1808_02950_b200 import adct, catalog
     m = adct.Matrix.from_int(catalog.T1, "T1")
     out = []
-    for (n, h, w) in [(2, 24, 272), (1, 2160, 3840), (3, 1080, 1920)]:
+    for (n, h, w) in [(2, 24, 272), (1, 2160, 3840), (3, 1080, 1920), (2, 40, 1280), (1, 136, 384)]:
         img = synth.ar1_field(n, h, w, 0.95, seed=h + w)
         out.append(adct.approx_dct8x8_fused_sse(m, img.cuda(), [10]).cpu().numpy().ravel())
     np.save(sys.argv[1], np.concatenate(out))
 """)
 
 
-@pytest.mark.parametrize("env", [{}, {"ADCT_DISABLE_STREAM": "1"}])
+@pytest.mark.parametrize("env", [{}, {"ADCT_DISABLE_STREAM": "1"}, {"ADCT_HOT": "simt"}, {"ADCT_TC_CW": "1"},
+                                 {"ADCT_TC_CW": "16"}])
 def test_kernel_variants_agree_with_oracle(tmp_path, env):
+    """Every kernel variant on the same geometries: the tensor-core kernel with its automatic tile
+    shape and with forced 1- and 16-chunk-wide tiles; the SIMT streaming kernel; the generic fused
+    kernels."""
     script = tmp_path / "v.py"
     script.write_text(_VARIANT_SCRIPT.format(root=ROOT))
     out = tmp_path / "o.npy"
@@ -135,7 +139,7 @@ def test_kernel_variants_agree_with_oracle(tmp_path, env):
     subprocess.run([sys.executable, str(script), str(out)], check=True, env=e, timeout=600)
     got = np.load(out)
     ref = []
-    for (n, h, w) in [(2, 24, 272), (1, 2160, 3840), (3, 1080, 1920)]:
+    for (n, h, w) in [(2, 24, 272), (1, 2160, 3840), (3, 1080, 1920), (2, 40, 1280), (1, 136, 384)]:
         img = synth.ar1_field(n, h, w, 0.95, seed=h + w)
         ref.append(oracle.codec_sse(img.numpy(), [10], t=M.T1).ravel())
     _check(got, np.concatenate(ref))
