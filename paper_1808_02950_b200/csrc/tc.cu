@@ -83,7 +83,74 @@ __host__ __device__ constexpr int nz_index(int p) {
   return popc64t(NZ & ((p == 0) ? 0ull : (~0ull >> (64 - p))));
 }
 
+#ifndef ADCT_TC_FFMA2
+#define ADCT_TC_FFMA2 0
+#endif
 __device__ __forceinline__ float i2f(uint32_t v) { return __int2float_rn((int32_t)v); }  // exact, |v| < 2^24
+
+// ---- packed fp32 (FFMA2 / FADD2, sm_100): two columns of a block per instruction -------------
+// The epilogue is issue-bound; a packed instruction does two FMAs for one issue slot (its pipe
+// occupancy is that of two), so pairing the vertical pass over column pairs cuts issued
+// instructions (the A/B in DESIGN.md §5.2).  Same roundings as the scalar code, per element.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+// c*x + acc for a compile-time coefficient c in {0, +-1, +-2, ...}
+template <class M>
+__device__ __forceinline__ float2 fmac2(float c, float2 x, float2 acc) {
+  if (M::kConst) {
+    if (c == 0.0f) return acc;
+    if (c == 1.0f) return __fadd2_rn(acc, x);
+    if (c == -1.0f) return __fadd2_rn(acc, f2(-x.x, -x.y));
+  }
+  return __ffma2_rn(f2(c, c), x, acc);
+}
+template <class M, uint32_t MASK, class C>
+__device__ __forceinline__ float2 lsum2(C c, const float2* x) {
+  int sd = -1;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (sd < 0 && ((MASK >> i) & 1u) && M::kConst && (c(i) == 1.0f || c(i) == -1.0f)) sd = i;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (sd < 0 && ((MASK >> i) & 1u) && (!M::kConst || c(i) != 0.0f)) sd = i;
+  if (sd < 0) return f2(0.0f, 0.0f);
+  float2 acc = (M::kConst && c(sd) == 1.0f) ? x[sd]
+               : ((M::kConst && c(sd) == -1.0f) ? f2(-x[sd].x, -x[sd].y) : __fmul2_rn(f2(c(sd), c(sd)), x[sd]));
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i != sd && ((MASK >> i) & 1u)) acc = fmac2<M>(c(i), x[i], acc);
+  return acc;
+}
+template <class M, uint32_t MASK, class C>
+__device__ __forceinline__ float2 lsub2(float2 acc, C c, const float2* x) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if ((MASK >> i) & 1u) acc = fmac2<M>(-c(i), x[i], acc);
+  return acc;
+}
+// the even half e_i of x = H y (inv8_e) for a column pair
+template <class M, uint32_t NZ>
+__device__ __forceinline__ void inv8_e2(const M& m, const float2* y, float2* e) {
+  constexpr uint32_t EV = NZ & 0x55u;
+  constexpr int nev = ((EV & 1u) ? 1 : 0) + ((EV & 4u) ? 1 : 0) + ((EV & 16u) ? 1 : 0) + ((EV & 64u) ? 1 : 0);
+  if constexpr (nev <= 2) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) e[i] = lsum2<M, EV>([&](int k) { return m.h(i, k); }, y);
+  } else {
+    float2 ee[2], eo[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      ee[i] = lsum2<M, NZ & 0x11u>([&](int k) { return m.h(i, k); }, y);
+      eo[i] = lsum2<M, NZ & 0x44u>([&](int k) { return m.h(i, k); }, y);
+    }
+    e[0] = __fadd2_rn(ee[0], eo[0]);
+    e[3] = __fadd2_rn(ee[0], f2(-eo[0].x, -eo[0].y));
+    e[1] = __fadd2_rn(ee[1], eo[1]);
+    e[2] = __fadd2_rn(ee[1], f2(-eo[1].x, -eo[1].y));
+  }
+}
+#ifndef ADCT_TC_PACKED
+#define ADCT_TC_PACKED 1
+#endif
 
 // ---- one block from its D row (s32 in registers): fp32 inverse and squared error ------------
 // yr: the NY coefficient columns; st: s_i[j] at 8j + i, t_i[j] at 8j + 4 + i (unused for r > 32)
@@ -111,6 +178,36 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
 #undef ADCT_TC_ROWINV
   }
   float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#if ADCT_TC_FFMA2
+  float2 acc2[4] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+#endif
+#if ADCT_TC_PACKED
+  if constexpr (!S::RESID) {
+    // vertical inverse fused with the error, two columns (j, j + 1) per packed instruction
+    float2 a2[4] = {f2(0.0f, 0.0f), f2(0.0f, 0.0f), f2(0.0f, 0.0f), f2(0.0f, 0.0f)};
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      const int j0 = 2 * jp, j1 = 2 * jp + 1;
+      float2 col[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) col[k] = ((ROWS >> k) & 1u) ? f2(q[k][j0], q[k][j1]) : f2(0.0f, 0.0f);
+      float2 e[4];
+      inv8_e2<MP, ROWS>(m, col, e);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 sv = f2(i2f(st[8 * j0 + i]), i2f(st[8 * j1 + i]));
+        const float2 tv = f2(i2f(st[8 * j0 + 4 + i]), i2f(st[8 * j1 + 4 + i]));
+        const float2 dp = __fadd2_rn(sv, f2(-e[i].x, -e[i].y));
+        const float2 dm = lsub2<MP, ROWS & 0xaau>(tv, [&](int k) { return m.h(i, k); }, col);
+        a2[i] = __ffma2_rn(dp, dp, a2[i]);
+        a2[i] = __ffma2_rn(dm, dm, a2[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = a2[i].x + a2[i].y;
+    return 0.5f * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+  }
+#endif
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     float col[8];
@@ -131,11 +228,21 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
       for (int i = 0; i < 4; ++i) {
         const float dp = i2f(st[8 * j + i]) - e[i];
         const float dm = lsub<MP, 8, ROWS & 0xaau>(i2f(st[8 * j + 4 + i]), [&](int k) { return m.h(i, k); }, col);
+#if ADCT_TC_FFMA2  // A/B: the two squares as one packed FFMA2 (half the issued instructions, same datapath)
+        acc2[i] = __ffma2_rn(make_float2(dp, dm), make_float2(dp, dm), acc2[i]);
+#else
         acc[i] = fmaf(dp, dp, acc[i]);
         acc[i] = fmaf(dm, dm, acc[i]);
+#endif
       }
     }
   }
+#if ADCT_TC_FFMA2
+  if constexpr (!S::RESID) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = acc2[i].x + acc2[i].y;
+  }
+#endif
   return 0.5f * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
 }
 

@@ -119,3 +119,27 @@ def test_sharded_table_equals_one_rank_and_oracle(world, one_rank_table):
         npix = p.shape[1] * p.shape[2]
         for f in range(N_FRAMES):
             assert abs(one_rank_table[f, len(planes) + i] - oracle.psnr(ref[f], npix)) <= 1e-3
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_second_device_after_first():
+    """Per-device lazy setup (function attributes, the sweep kernel's __constant__ zig-zag table,
+    the host pipeline's copy stream): the same calls on cuda:1 after cuda:0 give the same results
+    (ADVICE r1)."""
+    from paper_1808_02950_b200 import adct, catalog
+    m = adct.Matrix.from_int(catalog.T1, "T1")
+    img = synth.ar1_field(2, 64, 256, 0.95, seed=8)
+    out = []
+    for d in (0, 1):
+        with torch.cuda.device(d):
+            x = img.to(f"cuda:{d}")
+            sweep = adct.approx_dct8x8_fused_sse(m, x, [1, 10, 30]).cpu()      # sweep kernel (c_zz)
+            hot = adct.approx_dct8x8_fused_sse(m, x, [10]).cpu()               # tensor-core kernel
+            rt = adct.approx_dct8x8_roundtrip(m, x[:, :, :64].contiguous(), 10, torch.int16).cpu()
+            host = img.pin_memory()
+            ws = torch.empty(adct.host_workspace_bytes(adct.geom_of(host), 1, 1), dtype=torch.uint8,
+                             device=f"cuda:{d}")
+            h = adct.approx_dct8x8_fused_sse_host(m, host, [10], ws, chunk_images=1)
+            out.append((sweep, hot, rt, h))
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a, b)
