@@ -192,7 +192,9 @@ constexpr int kTcMaxPlanes = 3;                   // planes per approx_dct8x8_fu
 constexpr int kTcPartials = 4 * kTcEpi;           // partials per chunk
 constexpr int kTcBBytes = 160 * 128;              // B: N <= 160 outputs x K = 128 s8
 constexpr int kTcBars = 2 * kTcSlots + 4 * kTcDStages;
-constexpr size_t kTcSmem = (size_t)kTcSlots * kTcTileBytes + kTcBBytes + (size_t)kTcBars * 8 + 16 + 1024;
+constexpr int kTcBiasA = 128 * 16 * 2, kTcBiasB = 96 * 16 * 2;  // f16 constant tiles of the bias MMA (tc.cu)
+constexpr size_t kTcSmem = (size_t)kTcSlots * kTcTileBytes + kTcBBytes + (size_t)kTcBars * 8 + 16 + 128 + kTcBiasA +
+                           kTcBiasB + 1024;
 static_assert(kTcSmem <= 227 * 1024, "tensor-core kernel exceeds shared memory");
 struct TcPlan {
   int32_t cw;        // tile width in 128-byte chunks (16 / cw bands high)

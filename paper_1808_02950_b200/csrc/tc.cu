@@ -86,7 +86,20 @@ __host__ __device__ constexpr int nz_index(int p) {
 #ifndef ADCT_TC_FFMA2
 #define ADCT_TC_FFMA2 0
 #endif
+// s32 accumulator -> fp32.  ADCT_TC_FBIAS: every accumulator starts at 12582912.0f = 1.5 * 2^23
+// (one kind::f16 MMA of two constant tiles, 16 x 1024 x 768, written as f32 bits); the kind::i8
+// MMAs then add the integer result to that bit pattern, so D = 0x4B400000 + v is the fp32 number
+// 12582912 + v exactly (|v| < 2^22) and the conversion is one subtraction -- packed (FADD2) for
+// two values, where I2FP converts one per issue slot.  The epilogue is issue-bound.
+#ifndef ADCT_TC_FBIAS
+#define ADCT_TC_FBIAS 0  // the f16 bias MMA measured 10 % slower
+#endif
+constexpr float kTcMagic = 12582912.0f;
+#if ADCT_TC_FBIAS
+__device__ __forceinline__ float i2f(uint32_t v) { return __uint_as_float(v) - kTcMagic; }  // exact
+#else
 __device__ __forceinline__ float i2f(uint32_t v) { return __int2float_rn((int32_t)v); }  // exact, |v| < 2^24
+#endif
 
 // ---- packed fp32 (FFMA2 / FADD2, sm_100): two columns of a block per instruction -------------
 // The epilogue is issue-bound; a packed instruction does two FMAs for one issue slot (its pipe
@@ -148,9 +161,59 @@ __device__ __forceinline__ void inv8_e2(const M& m, const float2* y, float2* e) 
     e[2] = __fadd2_rn(ee[1], f2(-eo[1].x, -eo[1].y));
   }
 }
+// sum over l in MASK of z_l * (c(0, l), c(1, l)) for scalar z (two outputs per instruction)
+template <class M, uint32_t MASK, class C>
+__device__ __forceinline__ float2 psum2(C c, const float* z) {
+  float2 acc = f2(0.0f, 0.0f);
+  bool first = true;
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    if (!((MASK >> l) & 1u)) continue;
+    const float a = c(0, l), b = c(1, l);
+    if (M::kConst && a == 0.0f && b == 0.0f) continue;
+    const float2 zz = f2(z[l], z[l]);
+    if (first) {
+      acc = (M::kConst && a == 1.0f && b == 1.0f) ? zz : __fmul2_rn(f2(a, b), zz);
+      first = false;
+    } else {
+      acc = (M::kConst && a == 1.0f && b == 1.0f) ? __fadd2_rn(acc, zz) : __ffma2_rn(f2(a, b), zz, acc);
+    }
+  }
+  return acc;
+}
+// x = H z (one row of the horizontal inverse) as the column pairs (x0,x1), (x2,x3), (x4,x5),
+// (x6,x7): e_i over the even inputs, o_i over the odd ones, x_i = e_i + o_i, x_(7-i) = e_i - o_i
+template <class M, uint32_t NZ>
+__device__ __forceinline__ void inv8_pairs(const M& m, const float* z, float2* x) {
+  const float2 e01 = psum2<M, NZ & 0x55u>([&](int i, int l) { return m.h(i, l); }, z);
+  const float2 e23 = psum2<M, NZ & 0x55u>([&](int i, int l) { return m.h(2 + i, l); }, z);
+  const float2 o01 = psum2<M, NZ & 0xaau>([&](int i, int l) { return m.h(i, l); }, z);
+  const float2 o23 = psum2<M, NZ & 0xaau>([&](int i, int l) { return m.h(2 + i, l); }, z);
+  x[0] = __fadd2_rn(e01, o01);
+  x[1] = __fadd2_rn(e23, o23);
+  const float2 d23 = __fadd2_rn(e23, f2(-o23.x, -o23.y)), d01 = __fadd2_rn(e01, f2(-o01.x, -o01.y));
+  x[2] = f2(d23.y, d23.x);  // (x4, x5) = (e3 - o3, e2 - o2)
+  x[3] = f2(d01.y, d01.x);  // (x6, x7) = (e1 - o1, e0 - o0)
+}
 #ifndef ADCT_TC_PACKED
-#define ADCT_TC_PACKED 1
+#define ADCT_TC_PACKED 1  // 1: packed vertical pass; 2: the horizontal pass too (measured 1.5 % slower)
 #endif
+// two adjacent accumulators (a pair of s_i / t_i values, laid out as neighbours by tcB) as fp32
+__device__ __forceinline__ float2 i2f2(uint32_t a, uint32_t b) {
+#if ADCT_TC_FBIAS
+  return __fadd2_rn(f2(__uint_as_float(a), __uint_as_float(b)), f2(-kTcMagic, -kTcMagic));
+#else
+  return f2(i2f(a), i2f(b));
+#endif
+}
+// D column of s_i[j] (t = 0) / t_i[j] (t = 1) among the 64 butterfly columns: columns j = 2jp,
+// 2jp + 1 of the same (s/t, i) are neighbours, so a packed conversion reads an aligned pair
+#ifndef ADCT_TC_STPAIR
+#define ADCT_TC_STPAIR 1
+#endif
+__host__ __device__ constexpr int st_col(int j, int i, int t) {
+  return ADCT_TC_STPAIR ? 16 * (j >> 1) + 8 * t + 2 * i + (j & 1) : 8 * j + 4 * t + i;
+}
 
 // ---- one block from its D row (s32 in registers): fp32 inverse and squared error ------------
 // yr: the NY coefficient columns; st: s_i[j] at 8j + i, t_i[j] at 8j + 4 + i (unused for r > 32)
@@ -183,6 +246,26 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
 #endif
 #if ADCT_TC_PACKED
   if constexpr (!S::RESID) {
+#if ADCT_TC_PACKED >= 2
+    // the horizontal inverse again, straight into column pairs (q above is then dead code)
+    float2 q2[8][4];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (!((ROWS >> k) & 1u)) continue;
+      float z[8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? i2f(yr[nz_index<NZ>(k * 8 + l)]) * m.wy2(k, l) : 0.0f;
+#define ADCT_TC_ROWINV2(K)                                             \
+  if (k == K) {                                                        \
+    constexpr uint32_t rm = (uint32_t)((NZ >> (8 * K)) & 0xffull);     \
+    if constexpr (rm != 0) inv8_pairs<MP, rm>(m, z, q2[K]);            \
+  }
+      ADCT_TC_ROWINV2(0) ADCT_TC_ROWINV2(1) ADCT_TC_ROWINV2(2) ADCT_TC_ROWINV2(3)
+      ADCT_TC_ROWINV2(4) ADCT_TC_ROWINV2(5) ADCT_TC_ROWINV2(6) ADCT_TC_ROWINV2(7)
+#undef ADCT_TC_ROWINV2
+    }
+#endif
     // vertical inverse fused with the error, two columns (j, j + 1) per packed instruction
     float2 a2[4] = {f2(0.0f, 0.0f), f2(0.0f, 0.0f), f2(0.0f, 0.0f), f2(0.0f, 0.0f)};
 #pragma unroll
@@ -190,13 +273,18 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
       const int j0 = 2 * jp, j1 = 2 * jp + 1;
       float2 col[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) col[k] = ((ROWS >> k) & 1u) ? f2(q[k][j0], q[k][j1]) : f2(0.0f, 0.0f);
+      for (int k = 0; k < 8; ++k)
+#if ADCT_TC_PACKED >= 2
+        col[k] = ((ROWS >> k) & 1u) ? q2[k][jp] : f2(0.0f, 0.0f);
+#else
+        col[k] = ((ROWS >> k) & 1u) ? f2(q[k][j0], q[k][j1]) : f2(0.0f, 0.0f);
+#endif
       float2 e[4];
       inv8_e2<MP, ROWS>(m, col, e);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float2 sv = f2(i2f(st[8 * j0 + i]), i2f(st[8 * j1 + i]));
-        const float2 tv = f2(i2f(st[8 * j0 + 4 + i]), i2f(st[8 * j1 + 4 + i]));
+        const float2 sv = i2f2(st[st_col(j0, i, 0)], st[st_col(j1, i, 0)]);
+        const float2 tv = i2f2(st[st_col(j0, i, 1)], st[st_col(j1, i, 1)]);
         const float2 dp = __fadd2_rn(sv, f2(-e[i].x, -e[i].y));
         const float2 dm = lsub2<MP, ROWS & 0xaau>(tv, [&](int k) { return m.h(i, k); }, col);
         a2[i] = __ffma2_rn(dp, dp, a2[i]);
@@ -226,8 +314,8 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
       inv8_e<MP, ROWS>(m, col, e);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float dp = i2f(st[8 * j + i]) - e[i];
-        const float dm = lsub<MP, 8, ROWS & 0xaau>(i2f(st[8 * j + 4 + i]), [&](int k) { return m.h(i, k); }, col);
+        const float dp = i2f(st[st_col(j, i, 0)]) - e[i];
+        const float dm = lsub<MP, 8, ROWS & 0xaau>(i2f(st[st_col(j, i, 1)]), [&](int k) { return m.h(i, k); }, col);
 #if ADCT_TC_FFMA2  // A/B: the two squares as one packed FFMA2 (half the issued instructions, same datapath)
         acc2[i] = __ffma2_rn(make_float2(dp, dm), make_float2(dp, dm), acc2[i]);
 #else
@@ -315,6 +403,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* dfull = sfree + kTcSlots;                             // [2D] MMA done writing a half-stage
   uint64_t* dfree = dfull + 2 * kTcDStages;                       // [2D] half-stage read by 4 epilogue warps
   uint32_t* holder = reinterpret_cast<uint32_t*>(dfree + 2 * kTcDStages);
+#if ADCT_TC_FBIAS
+  // the two constant f16 operands of the bias MMA: A' = 1024 (128 rows x 16), B' = 768 (96 x 16)
+  uint32_t* cbias = reinterpret_cast<uint32_t*>(
+      smem + (((size_t)kTcSlots * kTcTileBytes + kTcBBytes + (size_t)kTcBars * 8 + 16 + 127) & ~(size_t)127));
+  for (int i = threadIdx.x; i < (kTcBiasA + kTcBiasB) / 4; i += kTcThreads)
+    cbias[i] = i < kTcBiasA / 4 ? 0x64006400u : 0x62006200u;
+#endif
   const MP m(dm);
 
   // B in the canonical K-major no-swizzle layout: core matrix (n/8, k/16) at (n/8)*1024 + (k/16)*128;
@@ -330,9 +425,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           pl = p & 7;
           break;
         }
-    } else if (o >= S::NY) {
-      sj = (o - S::NY) >> 3;  // column j of s_r / t_(r-4)
-      sr = (o - S::NY) & 7;
+    } else if (o >= S::NY) {  // inverse of st_col: column j of s_r (sr < 4) / t_(sr-4)
+      const int idx = o - S::NY;
+      sj = ADCT_TC_STPAIR ? 2 * (idx >> 4) + (idx & 1) : idx >> 3;
+      sr = ADCT_TC_STPAIR ? 4 * ((idx >> 3) & 1) + ((idx >> 1) & 3) : idx & 7;
     }
 #pragma unroll 1
     for (int i = 0; i < 8; ++i) {
@@ -395,6 +491,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t iss = (uint32_t)(w - kTcEpiWarps);
     // descriptors of slot 0 / k-step 0: the others differ only in the start address (bits 0-13)
     const uint64_t adesc0 = smem_desc_kmajor(ring0, 128, 1024), bdesc0 = smem_desc_kmajor(sB_u, 128, 1024);
+#if ADCT_TC_FBIAS
+    // uniform constant tiles: any layout reads the same values (LBO 128, SBO 256 stay inside)
+    const uint64_t adescc = smem_desc_kmajor(smem_u32(cbias), 128, 256);
+    const uint64_t bdescc = smem_desc_kmajor(smem_u32(cbias) + kTcBiasA, 128, 256);
+    constexpr uint32_t kIdescF16 = idesc_f16_f32<128, NB>();
+#endif
     uint32_t t = 0;
 #pragma unroll 1
     for (uint32_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
@@ -419,10 +521,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (h == 1) mbar_arrive(&sfree[slot]);
 #else
             const uint32_t td = tbase + (uint32_t)NB * hs;
+#if ADCT_TC_FBIAS
+            mma_f16_ss(td, adescc, bdescc, kIdescF16, 0u);  // D := 16 x 1024 x 768 = 1.5 * 2^23 (f32 bits)
+#endif
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               mma_i8_ss(td, ad + (uint64_t)(kk * 16), bdesc0 + (uint64_t)(h * (NB / 8) * 64 + kk * 16), kIdesc,
-                        kk > 0 ? 1u : 0u);
+                        (ADCT_TC_FBIAS || kk > 0) ? 1u : 0u);
             mma_commit(smem_u32(&dfull[hs]));                // half h of tile tt written
             if (h == 1) mma_commit(smem_u32(&sfree[slot]));  // the slot may be refilled
 #endif
