@@ -18,6 +18,13 @@
 
 #include "adct_host.h"
 #include "tma.cuh"
+#include "packed.cuh"
+
+// ADCT_BM_PACKED: the round trip of the block-major kernel on column pairs with packed fp32
+// (packed.cuh); 0 = the scalar networks (A/B)
+#ifndef ADCT_BM_PACKED
+#define ADCT_BM_PACKED 1
+#endif
 
 namespace adct {
 namespace {
@@ -96,8 +103,20 @@ __global__ void __launch_bounds__(32 * bm_warps<F32OUT>(), 1)
   uint32_t phase = 0;
   for (uint32_t t = wid; t < n_tiles; t += nw) {
     mbar_wait(&bars[slot], phase);
-    float x[8][8], y[8][8];
+    float x[8][8];
     const uint32_t ib = wbase + slot * 4096;
+#if ADCT_BM_PACKED
+    float2 x2[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 v = lds128(ib + swz(lane, i));
+      i16x2_to_f(v.x, x2[i][0].x, x2[i][0].y);
+      i16x2_to_f(v.y, x2[i][1].x, x2[i][1].y);
+      i16x2_to_f(v.z, x2[i][2].x, x2[i][2].y);
+      i16x2_to_f(v.w, x2[i][3].x, x2[i][3].y);
+    }
+#else
+    float y[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint4 v = lds128(ib + swz(lane, i));
@@ -106,16 +125,28 @@ __global__ void __launch_bounds__(32 * bm_warps<F32OUT>(), 1)
       i16x2_to_f(v.z, x[i][4], x[i][5]);
       i16x2_to_f(v.w, x[i][6], x[i][7]);
     }
+#endif
     __syncwarp();
     fence_proxy_async();
     if (pt < n_tiles) issue(slot);  // the slot's data is in registers: refill it now
     if (++slot == kBmInSlots) { slot = 0; phase ^= 1u; }
+#if ADCT_BM_PACKED
+    roundtrip2d_p(m, x2, wk.w);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        x[i][2 * c] = x2[i][c].x;
+        x[i][2 * c + 1] = x2[i][c].y;
+      }
+#else
     fwd2d(m, x, y);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
 #pragma unroll
       for (int l = 0; l < 8; ++l) y[k][l] *= wk.w[k * 8 + l];
     inv2d<MP, ~0ull>(m, y, x);
+#endif
     // the staging tile is free once the previous tile's store has read it
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
