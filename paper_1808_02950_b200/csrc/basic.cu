@@ -10,6 +10,13 @@
 #include <type_traits>
 
 #include "adct_host.h"
+#include "packed.cuh"
+
+// ADCT_RT_PACKED: the round trips of roundtrip_kernel and ssim_fused_kernel on column pairs with
+// packed fp32 (packed.cuh); 0 = the scalar networks (A/B)
+#ifndef ADCT_RT_PACKED
+#define ADCT_RT_PACKED 1
+#endif
 
 namespace adct {
 
@@ -204,14 +211,35 @@ __global__ void __launch_bounds__(256) roundtrip_kernel(const SrcT* __restrict__
                                                         int clip, float lo, float hi, void* __restrict__ recon) {
   const MP m(dm);
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += gridDim.x * blockDim.x) {
-    float x[8][8], y[8][8];
+    float x[8][8];
     load_block(src, g, b, dnbi, dbw, x);
-    fwd2d(m, x, y);
+#if ADCT_RT_PACKED
+    {
+      float2 x2[8][4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int l = 0; l < 8; ++l) y[k][l] *= wk.w[k * 8 + l];
-    inv2d<MP, ~0ull>(m, y, x);
+        for (int c = 0; c < 4; ++c) x2[i][c] = pk(x[i][2 * c], x[i][2 * c + 1]);
+      roundtrip2d_p(m, x2, wk.w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          x[i][2 * c] = x2[i][c].x;
+          x[i][2 * c + 1] = x2[i][c].y;
+        }
+    }
+#else
+    {
+      float y[8][8];
+      fwd2d(m, x, y);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int l = 0; l < 8; ++l) y[k][l] *= wk.w[k * 8 + l];
+      inv2d<MP, ~0ull>(m, y, x);
+    }
+#endif
     const uint32_t img = fdiv(b, dnbi);
     const uint32_t q = b - img * g.nbi;
     const uint32_t by = fdiv(q, dbw);
@@ -490,18 +518,39 @@ __global__ void __launch_bounds__(32 * kSfWarps, ADCT_SF_MINB) ssim_fused_kernel
   const int32_t nchunks = (height + 63) / 64;
   for (int32_t c = 0; c < nchunks; ++c) {
     {  // round trip of the lane's block (the composition approx_dct8x8_roundtrip, F32, no clip)
-      float x[8][8], y[8][8];
+      float x[8][8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) Src<uint8_t>::to_f(raw[i], x[i]);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         *reinterpret_cast<uint2*>(&X[8 + 8 * brl + i][8 * (lane & 3)]) = raw[i];
-      fwd2d(m, x, y);
+#if ADCT_RT_PACKED
+      {
+        float2 x2[8][4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int l = 0; l < 8; ++l) y[k][l] *= wk.w[k * 8 + l];
-      inv2d<MP, ~0ull>(m, y, x);
+          for (int c = 0; c < 4; ++c) x2[i][c] = pk(x[i][2 * c], x[i][2 * c + 1]);
+        roundtrip2d_p(m, x2, wk.w);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            x[i][2 * c] = x2[i][c].x;
+            x[i][2 * c + 1] = x2[i][c].y;
+          }
+      }
+#else
+      {
+        float y[8][8];
+        fwd2d(m, x, y);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int l = 0; l < 8; ++l) y[k][l] *= wk.w[k * 8 + l];
+        inv2d<MP, ~0ull>(m, y, x);
+      }
+#endif
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float* d = &Y[8 + 8 * brl + i][8 * (lane & 3)];

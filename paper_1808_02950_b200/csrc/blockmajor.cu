@@ -284,7 +284,39 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
     __syncwarp();
 #pragma unroll 1
     for (int b = 0; b < 2; ++b) {
-      float x[8][8], y[8][8];
+      float y[8][8];
+#if ADCT_BM_PACKED  // forward on column pairs (packed.cuh), coefficients back in raster order
+      {
+        float2 x2[8][4], p2[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          x2[i][0] = pk(pxf_q<0x7504u>(rows[b][i].x, magic), pxf_q<0x7514u>(rows[b][i].x, magic));
+          x2[i][1] = pk(pxf_q<0x7524u>(rows[b][i].x, magic), pxf_q<0x7534u>(rows[b][i].x, magic));
+          x2[i][2] = pk(pxf_q<0x7504u>(rows[b][i].y, magic), pxf_q<0x7514u>(rows[b][i].y, magic));
+          x2[i][3] = pk(pxf_q<0x7524u>(rows[b][i].y, magic), pxf_q<0x7534u>(rows[b][i].y, magic));
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float2 col[8], out[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) col[i] = x2[i][c];
+          fwd8p(m, col, out);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) p2[k][c] = out[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float2 yq[4];
+          fwd8_row(m, p2[k], yq);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            y[k][yq_col(q, 0)] = yq[q].x;
+            y[k][yq_col(q, 1)] = yq[q].y;
+          }
+        }
+      }
+#else
+      float x[8][8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         x[i][0] = pxf_q<0x7504u>(rows[b][i].x, magic); x[i][1] = pxf_q<0x7514u>(rows[b][i].x, magic);
@@ -293,6 +325,7 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
         x[i][6] = pxf_q<0x7524u>(rows[b][i].y, magic); x[i][7] = pxf_q<0x7534u>(rows[b][i].y, magic);
       }
       fwd2d(m, x, y);
+#endif
       // quantise.  T1: c_kl = step * sqrt(n_k n_l) is an integer multiple of step unless exactly
       // one of k, l is in {2, 6} (n = 20 against 8 or 18); integer c is rounded exactly in fp32.
       bool near = false;

@@ -3,6 +3,12 @@
 #include "adct_host.h"
 #include "fused_common.cuh"
 
+// ADCT_SWEEP_PACKED: the rank-one updates and the squared error of CLIP_NONE on column pairs
+// (FFMA2: two pixels per issue slot, each element the same fma sequence as the scalar code)
+#ifndef ADCT_SWEEP_PACKED
+#define ADCT_SWEEP_PACKED 1
+#endif
+
 namespace adct {
 namespace {
 
@@ -45,6 +51,43 @@ __global__ void __launch_bounds__(NT) fused_sweep_kernel(const SrcT* __restrict_
 #pragma unroll
       for (int p = 0; p < 64; ++p) ys[p][threadIdx.x] = y[p >> 3][p & 7] * dm.wy[p];
     }
+#if ADCT_SWEEP_PACKED
+    if (clip == ADCT_CLIP_NONE) {
+      float2 e2[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) e2[i][c] = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+      for (int zr = 63; zr >= rmin && zr >= 1; --zr) {
+        const int pos = c_zz[zr];
+        const int k = pos >> 3, l = pos & 7;
+        const float cz = ys[pos][threadIdx.x];
+        float a[8];
+        float2 hl2[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = fmaf(dm.h[i * 8 + k], cz, -0.0f);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) hl2[c] = make_float2(dm.h[(2 * c) * 8 + l], dm.h[(2 * c + 1) * 8 + l]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) e2[i][c] = __ffma2_rn(hl2[c], make_float2(a[i], a[i]), e2[i][c]);
+        if ((rmask >> zr) & 1ull) {
+          float2 sa = make_float2(0.0f, 0.0f), sb = make_float2(0.0f, 0.0f);  // (s0, s1), (s2, s3)
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if (c & 1) sb = __ffma2_rn(e2[i][c], e2[i][c], sb);
+              else sa = __ffma2_rn(e2[i][c], e2[i][c], sa);
+            }
+          zacc[zr - 1][threadIdx.x] += (sa.x + sa.y) + (sb.x + sb.y);
+        }
+      }
+      continue;
+    }
+#endif
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
