@@ -19,6 +19,14 @@
 #include <mutex>
 
 #include "adct_host.h"
+#include "packed.cuh"
+
+// ADCT_JAM_PACKED: the N-point networks on consecutive element pairs with packed fp32 (FFMA2 /
+// FADD2; packed.cuh), coefficients in the permuted "slot" order the packed recursion produces
+// (the weight table is permuted to match on the host); 0 = the scalar networks (A/B)
+#ifndef ADCT_JAM_PACKED
+#define ADCT_JAM_PACKED 0  // packed: parity-green but no faster (4.56 vs 4.52 ms T(16)): the kernel is not FP-issue-bound
+#endif
 
 namespace adct {
 namespace {
@@ -78,6 +86,81 @@ struct Jam<8> {
     inv8<T1Mat, 0xffu>(T1Mat(g_jam_unused), y, x);
   }
 };
+
+// Packed JAM recursion.  In: N/2 consecutive pairs (x0,x1), (x2,x3), ...  Out: N/2 pairs in the
+// slot layout L_N -- L_8 is packed.cuh's yq layout (y0,y4), (y2,y6), (y1,y3), (y5,y7); L_N puts
+// the even outputs (T(N/2) of u, in L_(N/2)) in the first N/4 pairs and the odd ones (T(N/2) of
+// v) in the rest.  The inverse reads L_N and writes consecutive pairs.  The butterflies pair
+// element i with N-1-i, i.e. pair c with the swapped pair N/2-1-c.
+template <int N>
+struct JamP {
+  __device__ __forceinline__ static void fwd(const float2* x, float2* y) {
+    float2 u[N / 4], v[N / 4];
+#pragma unroll
+    for (int c = 0; c < N / 4; ++c) {
+      u[c] = padd(x[c], pswap(x[N / 2 - 1 - c]));
+      v[c] = psub(x[c], pswap(x[N / 2 - 1 - c]));
+    }
+    JamP<N / 2>::fwd(u, y);
+    JamP<N / 2>::fwd(v, y + N / 4);
+  }
+  __device__ __forceinline__ static void inv(const float2* y, float2* x) {
+    float2 a[N / 4], b[N / 4];
+    JamP<N / 2>::inv(y, a);
+    JamP<N / 2>::inv(y + N / 4, b);
+#pragma unroll
+    for (int c = 0; c < N / 4; ++c) {
+      x[c] = padd(a[c], b[c]);
+      x[N / 2 - 1 - c] = pswap(psub(a[c], b[c]));
+    }
+  }
+};
+template <>
+struct JamP<8> {
+  __device__ __forceinline__ static void fwd(const float2* x, float2* y) { fwd8_row(T1Mat(g_jam_unused), x, y); }
+  __device__ __forceinline__ static void inv(const float2* y, float2* x) { inv8_row(T1Mat(g_jam_unused), y, x); }
+};
+// scalar interface: x natural order -> y in slot order (float 2c + h of pair c), and back
+template <int N>
+struct JamPk {
+  __device__ __forceinline__ static void fwd(const float* x, float* y) {
+    float2 x2[N / 2], y2[N / 2];
+#pragma unroll
+    for (int c = 0; c < N / 2; ++c) x2[c] = pk(x[2 * c], x[2 * c + 1]);
+    JamP<N>::fwd(x2, y2);
+#pragma unroll
+    for (int c = 0; c < N / 2; ++c) {
+      y[2 * c] = y2[c].x;
+      y[2 * c + 1] = y2[c].y;
+    }
+  }
+  __device__ __forceinline__ static void inv(const float* y, float* x) {
+    float2 y2[N / 2], x2[N / 2];
+#pragma unroll
+    for (int c = 0; c < N / 2; ++c) y2[c] = pk(y[2 * c], y[2 * c + 1]);
+    JamP<N>::inv(y2, x2);
+#pragma unroll
+    for (int c = 0; c < N / 2; ++c) {
+      x[2 * c] = x2[c].x;
+      x[2 * c + 1] = x2[c].y;
+    }
+  }
+};
+#if ADCT_JAM_PACKED
+template <int N>
+using JamNet = JamPk<N>;
+#else
+template <int N>
+using JamNet = Jam<N>;
+#endif
+// host: slot of output frequency k in L_N (inverse of the layout above)
+inline int jam_slot(int n, int k) {
+  if (n == 8) {
+    constexpr int s8[8] = {0, 4, 2, 5, 1, 6, 3, 7};  // y0->0, y4->1, y2->2, y6->3, y1->4, y3->5, y5->6, y7->7
+    return s8[k];
+  }
+  return (k % 2 == 0) ? jam_slot(n / 2, k / 2) : n / 2 + jam_slot(n / 2, k / 2);
+}
 
 template <int N>
 struct JamW {
@@ -226,7 +309,7 @@ __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_M
     {  // pass 1: row i of block bl, forward
       float x[N], y[N];
       to_float<N>(raw, x);
-      Jam<N>::fwd(x, y);
+      JamNet<N>::fwd(x, y);
 #pragma unroll
       for (int j = 0; j < N; j += 4) *reinterpret_cast<float4*>(row + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
     }
@@ -240,7 +323,7 @@ __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_M
       float c[N], y[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) c[k] = sm[(bl * N + k) * P + i];
-      Jam<N>::fwd(c, y);
+      JamNet<N>::fwd(c, y);
 #pragma unroll
       for (int k = 0; k < N; k += 4) {
         const float4 w4 = *reinterpret_cast<const float4*>(sw + i * P + k);
@@ -249,7 +332,7 @@ __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_M
         y[k + 2] *= w4.z;
         y[k + 3] *= w4.w;
       }
-      Jam<N>::inv(y, c);
+      JamNet<N>::inv(y, c);
 #pragma unroll
       for (int k = 0; k < N; ++k) sm[(bl * N + k) * P + i] = c[k];
     }
@@ -264,7 +347,7 @@ __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_M
         z[j + 2] = r4.z;
         z[j + 3] = r4.w;
       }
-      Jam<N>::inv(z, x);
+      JamNet<N>::inv(z, x);
       if (valid && kSat16 && out_t == ADCT_I16) {  // int16 -> int16: the saturating pack is the clip
         store_row_any<N, true>(recon, off, out_t, x);
       } else if (valid) {
@@ -313,7 +396,11 @@ adct_status launch_jam(const void* src, const adct_geom& g, int32_t r, void* rec
   zigzag_keep<N>(r, keep);
   JamW<N> wt;
   for (int k = 0; k < N; ++k)
-    for (int l = 0; l < N; ++l) wt.w[k * N + l] = keep[k * N + l] ? (float)(1.0 / (d[k] * d[l])) : 0.0f;
+    for (int l = 0; l < N; ++l) {
+      // the kernel sees coefficient (k, l) at (slot(k), slot(l)) when the networks are packed
+      const int sk = ADCT_JAM_PACKED ? jam_slot(N, k) : k, sl = ADCT_JAM_PACKED ? jam_slot(N, l) : l;
+      wt.w[sk * N + sl] = keep[k * N + l] ? (float)(1.0 / (d[k] * d[l])) : 0.0f;
+    }
   KGeom kg;
   kg.image_stride = g.image_stride;
   kg.row_stride = g.row_stride;
