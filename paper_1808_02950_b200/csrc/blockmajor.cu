@@ -25,6 +25,11 @@
 #ifndef ADCT_BM_PACKED
 #define ADCT_BM_PACKED 1
 #endif
+// ADCT_Q_PACKED: the C3 quantiser itself on coefficient pairs -- parity-green but slower
+// (1.407 vs 1.291 ms per C3 step: the per-lane sign/select work does not pack), so off
+#ifndef ADCT_Q_PACKED
+#define ADCT_Q_PACKED 0
+#endif
 
 namespace adct {
 namespace {
@@ -330,6 +335,52 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
       // one of k, l is in {2, 6} (n = 20 against 8 or 18); integer c is rounded exactly in fp32.
       bool near = false;
       uint32_t packed[32];
+#if ADCT_Q_PACKED
+      // two coefficients per packed instruction, paired as the packed forward leaves them: slots
+      // (0,4), (2,6), (1,3), (5,7) of a row, which are both rational or both irrational.  Same
+      // fp32 operations per element as the scalar code below, except that the correction
+      // m0 - [rem < 0] is formed as (m0 + copysign(0.5, rem)) - 0.5 (exact: rem is an exact
+      // integer, +0 when it vanishes) instead of a compare and select
+      {
+        uint32_t u[8][8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int la = yq_col(q, 0), lb = yq_col(q, 1);
+            const float2 yy = pk(y[k][la] - ((k == 0 && la == 0) ? 64.0f * 32768.0f : 0.0f), y[k][lb]);  // exact
+            y[k][la] = yy.x;
+            y[k][lb] = yy.y;
+            const float2 inv = pk(qt.inv[k * 8 + la], qt.inv[k * 8 + lb]);
+            if (t1_rational(k, la)) {
+              const float ca = stepf * (float)t1_sqrt_nn(k, la), cb = stepf * (float)t1_sqrt_nn(k, lb);
+              const float2 A = __fadd2_rn(pk(fabsf(yy.x), fabsf(yy.y)), pk(0.5f * ca, 0.5f * cb));
+              const float2 f = __ffma2_rn(A, inv, pk(12582912.0f, 12582912.0f));
+              const float2 m0 = __fadd2_rn(f, pk(-12582912.0f, -12582912.0f));
+              const float2 rem = __ffma2_rn(pk(-ca, -cb), m0, A);
+              const float2 hs = pk(__uint_as_float(0x3F000000u | (__float_as_uint(rem.x) & 0x80000000u)),
+                                   __uint_as_float(0x3F000000u | (__float_as_uint(rem.y) & 0x80000000u)));
+              const float2 mf = __fadd2_rn(__fadd2_rn(m0, hs), pk(-0.5f, -0.5f));
+              const float2 qf = pk(__uint_as_float(__float_as_uint(mf.x) | (__float_as_uint(yy.x) & 0x80000000u)),
+                                   __uint_as_float(__float_as_uint(mf.y) | (__float_as_uint(yy.y) & 0x80000000u)));
+              const float2 uu = __fadd2_rn(qf, pk(12582912.0f, 12582912.0f));
+              u[k][la] = __float_as_uint(uu.x);
+              u[k][lb] = __float_as_uint(uu.y);
+            } else {
+              const float2 v = __fmul2_rn(yy, inv);
+              const float2 f = __fadd2_rn(v, pk(12582912.0f, 12582912.0f));
+              const float2 d = __fadd2_rn(v, pk(-(f.x - 12582912.0f), -(f.y - 12582912.0f)));
+              near |= fabsf(d.x) > 0.49993896f || fabsf(d.y) > 0.49993896f;  // within 2^-14 of a boundary
+              u[k][la] = __float_as_uint(f.x);
+              u[k][lb] = __float_as_uint(f.y);
+            }
+          }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int l = 0; l < 8; l += 2) packed[k * 4 + l / 2] = __byte_perm(u[k][l], u[k][l + 1], 0x5410);
+      }
+#else
 #pragma unroll
       for (int k = 0; k < 8; ++k)
 #pragma unroll
@@ -359,6 +410,7 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
           }
           packed[k * 4 + l / 2] = __byte_perm(u[0], u[1], 0x5410);
         }
+#endif
       if (__any_sync(0xffffffffu, near)) {  // rare: exact integer rule at irrational positions
 #pragma unroll
         for (int kl = 0; kl < 64; ++kl) {
