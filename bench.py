@@ -486,6 +486,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--shard-of", default=None,
+                    help="q/W: run only rank q of W's share of the C4 stack on this one GPU (a scaling probe; "
+                         "value then counts the whole stack's blocks and is NOT a bench line)")
     ap.add_argument("--planes", action="store_true",
                     help="one approx_dct8x8_fused_sse_planes call per step (Y+U+V); the roofline event then "
                          "brackets the three planes")
@@ -511,7 +514,14 @@ def main():
     stream = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)  # the error-table all-reduce overlaps the next step's kernels
     m = adct.Matrix.from_int(catalog.T1, "T1")
-    if args.scaling == "strong":
+    if args.shard_of:
+        # scaling probe on ONE GPU (not a bench line): this process does exactly rank q of W's
+        # share of the 512-frame stack, e.g. --shard-of 0/8 = the 64 frames of one rank at 8 GPUs
+        q, wq = (int(v) for v in args.shard_of.split("/"))
+        n_total = FRAMES
+        lo, hi = parallel.shard_range(FRAMES, q, wq)
+        planes = make_frames(lo, hi, dev)
+    elif args.scaling == "strong":
         # BASELINE C4: ONE 512-frame stack sharded over the ranks, [floor(qN/W), floor((q+1)N/W))
         n_total = FRAMES
         lo, hi = parallel.shard_range(FRAMES, rank, world)

@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdint>
 #include <mutex>
+#include <utility>
 
 #include "adct.h"
 #include "adct_internal.cuh"
@@ -40,6 +41,39 @@ inline bool once_per_device(std::mutex& mu, int8_t (&state)[kMaxDevices], F&& f)
   std::lock_guard<std::mutex> lk(mu);
   if (state[dev] == 0) state[dev] = f() ? 1 : -1;
   return state[dev] == 1;
+}
+
+// Programmatic dependent launch (ADCT_PDL): the persistent stream kernels and their finalize are
+// launched with programmatic stream serialization, call griddepcontrol.launch_dependents at
+// entry and griddepcontrol.wait before their first global memory access, so a launch's
+// prologue (barrier init, TMEM allocation, the B operand) overlaps the previous kernel's tail
+// while every kernel still completes after the one before it.
+#ifndef ADCT_PDL
+#define ADCT_PDL 1
+#endif
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if ADCT_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if ADCT_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <typename... K, typename... A>
+inline cudaError_t launch_pdl(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ADCT_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
 }
 
 inline adct_status check_geom(const adct_geom& g) {
@@ -183,7 +217,16 @@ constexpr int kTcDStages = kTcWays;               // TMEM accumulator stages (N 
 #ifndef ADCT_TC_CHUNK
 #define ADCT_TC_CHUNK 24
 #endif
-constexpr int kTcChunkTiles = ADCT_TC_CHUNK;      // tiles per chunk
+constexpr int kTcChunkTiles = ADCT_TC_CHUNK;      // tiles per chunk, at most
+// tiles per chunk of a plane: from the image geometry only (so per-image sums do not depend on
+// how images are batched or sharded), small enough that an image has >= 32 chunks -- a 64-frame
+// chroma shard (8 GPUs) then still spreads over many waves of the 148 CTAs -- at least 4
+inline int32_t tc_chunk_tiles(int64_t tiles_per_image) {
+  int64_t c = tiles_per_image / 32;
+  if (c < 4) c = 4;
+  if (c > kTcChunkTiles) c = kTcChunkTiles;
+  return (int32_t)c;
+}
 constexpr int kTcMaxPlanes = 3;                   // planes per approx_dct8x8_fused_sse_planes call (Y, U, V)
 #ifndef ADCT_TC_ABL
 #define ADCT_TC_ABL 0  // ablation builds only (tools/build_variant.sh): 1 no epilogue math, 2 no TMEM load, 3 no MMA
@@ -199,6 +242,7 @@ static_assert(kTcSmem <= 227 * 1024, "tensor-core kernel exceeds shared memory")
 struct TcPlan {
   int32_t cw;        // tile width in 128-byte chunks (16 / cw bands high)
   int32_t tpr, tpi;  // tiles per tile row, per image
+  int32_t ct;        // tiles per chunk
   int32_t cpi;       // chunks per image
   int64_t n_chunks;
   bool ok;
@@ -210,7 +254,8 @@ inline int64_t stream_partials_per_image(const adct_geom& g) {
   if (g.width % 128 == 0) {  // tensor-core tiles (any of its shapes)
     for (int cw : {16, 2, 1}) {
       const int64_t tpi = ((g.width / 128 + cw - 1) / cw) * ((g.height / 8 + 16 / cw - 1) / (16 / cw));
-      const int64_t c = (tpi + kTcChunkTiles - 1) / kTcChunkTiles * kTcPartials;
+      const int64_t ct = tc_chunk_tiles(tpi);
+      const int64_t c = (tpi + ct - 1) / ct * kTcPartials;
       if (c > best) best = c;
     }
   }

@@ -300,6 +300,8 @@ __global__ void __launch_bounds__(kFinNT) finalize_kernel(const double* __restri
                                                           double* __restrict__ sse, double* __restrict__ psnr,
                                                           double scale) {
   __shared__ double red[kFinNT];
+  pdl_launch_dependents();
+  pdl_wait();  // the kernel that wrote the partials has completed
   const int64_t img = blockIdx.x;
   const int32_t o = blockIdx.y;
   const int32_t s = slot_of.s[o];
@@ -617,9 +619,8 @@ void launch_finalize_scaled(const double* partial, int32_t chunks, int64_t n_ima
 void launch_finalize(const double* partial, int32_t chunks, int64_t n_images, int32_t slots, const SlotMap& slot_of,
                      int32_t n_out, double npix, double peak, double* sse, double* psnr, cudaStream_t st) {
   if (n_images * n_out == 0) return;
-  finalize_kernel<<<dim3((unsigned)n_images, (unsigned)n_out), kFinNT, 0, st>>>(partial, chunks, n_images, slots,
-                                                                                slot_of, n_out, npix, peak, sse, psnr,
-                                                                                1.0);
+  launch_pdl(finalize_kernel, dim3((unsigned)n_images, (unsigned)n_out), dim3(kFinNT), 0, st, partial, chunks, n_images,
+             slots, slot_of, n_out, npix, peak, sse, psnr, 1.0);
   count_launch();
 }
 

@@ -77,6 +77,18 @@ struct TcShape {
   static_assert(N <= 256 && N % 16 == 0, "MMA N");
 };
 
+// T1 in constant memory for the B construction, where the row index is a runtime value (the
+// constexpr table of T1Mat would be copied to local memory there)
+__constant__ float c_t1f[64] = {1, 1, 1,  1,  1,  1,  1,  1,  2, 2,  1,  0,  0,  -1, -2, -2,
+                                2, 1, -1, -2, -2, -1, 1,  2,  1, 0,  -2, -2, 2,  2,  0,  -1,
+                                1, -1, -1, 1, 1,  -1, -1, 1,  2, -2, 0,  1,  -1, 0,  2,  -2,
+                                1, -2, 2, -1, -1, 2,  -2, 1,  0, -1, 2,  -2, 2,  -2, 1,  0};
+template <class MP>
+__device__ __forceinline__ float frt(const MP& m, int k, int i) {
+  if constexpr (MP::kConst) return c_t1f[k * 8 + i];
+  else return m.f(k, i);
+}
+
 // index of coefficient p = k*8+l among the set bits of NZ (its D column)
 template <uint64_t NZ>
 __host__ __device__ constexpr int nz_index(int p) {
@@ -338,14 +350,15 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
 // consecutive tiles of one image (fewer at the image's end), taken in order ------------------
 struct TcArgs {
   int32_t tpr, tpi, cpi;  // tiles per tile row, per image; chunks per image
+  int32_t ct;             // tiles per chunk (tc_chunk_tiles)
   uint32_t n_chunks;
   FastDiv dcpi, dtpr;
 };
 
 __device__ __forceinline__ int32_t chunk_tiles(const TcArgs& a, uint32_t cg, uint32_t& img, int32_t& tt0) {
   img = fdiv(cg, a.dcpi);
-  tt0 = (int32_t)(cg - img * (uint32_t)a.cpi) * kTcChunkTiles;
-  return min(kTcChunkTiles, a.tpi - tt0);
+  tt0 = (int32_t)(cg - img * (uint32_t)a.cpi) * a.ct;
+  return min(a.ct, a.tpi - tt0);
 }
 
 struct TcPf {  // the TMA producer's walk: coordinates of the next tile to load
@@ -395,6 +408,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   static_assert(2 * kTcDStages * NB <= (int)kTmemCols, "TMEM columns");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  pdl_launch_dependents();  // the next launch may start its prologue as our CTAs retire
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = w & 3;  // TMEM lane quarter of this warp (hardware: warp w accesses lanes 32 (w % 4) ..)
   uint8_t* sB = smem + (size_t)kTcSlots * kTcTileBytes;
@@ -413,12 +427,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const MP m(dm);
 
   // B in the canonical K-major no-swizzle layout: core matrix (n/8, k/16) at (n/8)*1024 + (k/16)*128;
-  // thread n writes row n, one 16-byte pixel row i (both blocks) at a time
-  for (int n = threadIdx.x; n < N; n += kTcThreads) {
+  // one thread per (output n, pixel row i) writes that 16-byte row (both blocks of the pair; the
+  // other block's 8 bytes are 0).  Part of every launch's ramp, so no local-memory arrays.
+  for (int idx = threadIdx.x; idx < N * 8; idx += kTcThreads) {
+    const int n = idx >> 3, i = idx & 7;
     const int blk = n / NB, o = n % NB;
     int pk = -1, pl = -1, sj = -1, sr = -1;
     if (o < S::NNZ) {
       int cnt = -1;
+#pragma unroll 1
       for (int p = 0; p < 64; ++p)
         if (((S::NZ >> p) & 1ull) && ++cnt == o) {
           pk = p >> 3;
@@ -426,23 +443,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           break;
         }
     } else if (o >= S::NY) {  // inverse of st_col: column j of s_r (sr < 4) / t_(sr-4)
-      const int idx = o - S::NY;
-      sj = ADCT_TC_STPAIR ? 2 * (idx >> 4) + (idx & 1) : idx >> 3;
-      sr = ADCT_TC_STPAIR ? 4 * ((idx >> 3) & 1) + ((idx >> 1) & 3) : idx & 7;
+      const int id = o - S::NY;
+      sj = ADCT_TC_STPAIR ? 2 * (id >> 4) + (id & 1) : id >> 3;
+      sr = ADCT_TC_STPAIR ? 4 * ((id >> 3) & 1) + ((id >> 1) & 3) : id & 7;
     }
-#pragma unroll 1
-    for (int i = 0; i < 8; ++i) {
-      uint32_t wv[4] = {0u, 0u, 0u, 0u};
+    const float fki = pk >= 0 ? frt(m, pk, i) : 0.0f;
+    uint32_t lo = 0u, hi = 0u;  // bytes j = 0..3 and 4..7 of this block's 8
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        int v = 0;
-        if (pk >= 0) v = (int)lrintf(m.f(pk, i) * m.f(pl, j));
-        else if (sj == j) v = sr < 4 ? ((i == sr || i == 7 - sr) ? 1 : 0) : (i == sr - 4 ? 1 : (i == 11 - sr ? -1 : 0));
-        const int c = 8 * blk + j;  // byte of the 16-byte pixel row of the pair
-        wv[c >> 2] |= ((uint32_t)(uint8_t)(int8_t)v) << (8 * (c & 3));
-      }
-      *reinterpret_cast<uint4*>(sB + (n >> 3) * 1024 + i * 128 + (n & 7) * 16) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    for (int j = 0; j < 8; ++j) {
+      int v = 0;
+      if (pk >= 0) v = (int)lrintf(fki * frt(m, pl, j));
+      else if (sj == j) v = sr < 4 ? ((i == sr || i == 7 - sr) ? 1 : 0) : (i == sr - 4 ? 1 : (i == 11 - sr ? -1 : 0));
+      const uint32_t b = (uint32_t)(uint8_t)(int8_t)v;
+      if (j < 4) lo |= b << (8 * j);
+      else hi |= b << (8 * (j - 4));
     }
+    *reinterpret_cast<uint4*>(sB + (n >> 3) * 1024 + i * 128 + (n & 7) * 16) =
+        blk ? make_uint4(0u, 0u, lo, hi) : make_uint4(lo, hi, 0u, 0u);
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kTcSlots; ++i) {
@@ -461,6 +478,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *holder;
+  pdl_wait();  // the previous kernel of the stream has completed: inputs ready, partials free
   const uint32_t full0 = smem_u32(full), ring0 = smem_u32(smem), sB_u = smem_u32(sB);
 
   if (w == kTcEpiWarps + kTcIssuers) {
@@ -609,7 +627,9 @@ bool launch_tc_rc(const CUtensorMap& map, const TcArgs& a, const DevMat& dm, dou
       }))
     return false;
   const int64_t grid = (int64_t)a.n_chunks < sms_s() ? (int64_t)a.n_chunks : sms_s();
-  fused_u8_tc_kernel<MP, R, CW><<<(unsigned)grid, kTcThreads, kTcSmem, st>>>(map, a, dm, partial);
+  if (launch_pdl(fused_u8_tc_kernel<MP, R, CW>, dim3((unsigned)grid), dim3(kTcThreads), kTcSmem, st, map, a, dm,
+                 partial) != cudaSuccess)
+    return false;
   return true;
 }
 
@@ -680,7 +700,8 @@ TcPlan tc_plan(const adct_geom& g) {
   }
   p.tpr = (int32_t)((nch + p.cw - 1) / p.cw);
   p.tpi = (int32_t)(p.tpr * ((nbd + 16 / p.cw - 1) / (16 / p.cw)));
-  p.cpi = (p.tpi + kTcChunkTiles - 1) / kTcChunkTiles;
+  p.ct = tc_chunk_tiles(p.tpi);
+  p.cpi = (p.tpi + p.ct - 1) / p.ct;
   p.n_chunks = g.n_images * (int64_t)p.cpi;
   p.ok = (g.row_stride % 16) == 0 && (g.n_images <= 1 || (g.image_stride % 16) == 0) &&
          g.image_stride < ((int64_t)1 << 40) && 8 * g.row_stride < ((int64_t)1 << 40) &&
@@ -700,6 +721,7 @@ bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, i
   a.tpr = p.tpr;
   a.tpi = p.tpi;
   a.cpi = p.cpi;
+  a.ct = p.ct;
   a.n_chunks = (uint32_t)p.n_chunks;
   a.dcpi = make_fastdiv((uint32_t)p.cpi);
   a.dtpr = make_fastdiv((uint32_t)p.tpr);
