@@ -240,7 +240,8 @@ constexpr size_t kTcSmem = (size_t)kTcSlots * kTcTileBytes + kTcBBytes + (size_t
                            kTcBiasB + 1024;
 static_assert(kTcSmem <= 227 * 1024, "tensor-core kernel exceeds shared memory");
 struct TcPlan {
-  int32_t cw;        // tile width in 128-byte chunks (16 / cw bands high)
+  int32_t cw;        // tile width in 128-byte chunks (16 / cw bands high); 15: donor tiling (tc.cu)
+  int32_t dmain, dlast, dc0;  // donor tiling: main tiles per image, leftover tile's band and first chunk
   int32_t tpr, tpi;  // tiles per tile row, per image
   int32_t ct;        // tiles per chunk
   int32_t cpi;       // chunks per image

@@ -353,6 +353,7 @@ struct TcArgs {
   int32_t ct;             // tiles per chunk (tc_chunk_tiles)
   uint32_t n_chunks;
   FastDiv dcpi, dtpr;
+  int32_t dmain, dlast, dc0;  // donor tiles (CW = 15): main tiles per image; the leftover tile's band, first chunk
 };
 
 __device__ __forceinline__ int32_t chunk_tiles(const TcArgs& a, uint32_t cg, uint32_t& img, int32_t& tt0) {
@@ -364,6 +365,7 @@ __device__ __forceinline__ int32_t chunk_tiles(const TcArgs& a, uint32_t cg, uin
 struct TcPf {  // the TMA producer's walk: coordinates of the next tile to load
   uint32_t cg, img;
   int32_t j, n, trow, tcol;
+  int32_t dband, dchunk;  // donor tiles: the donor chunk-band of tile trow
 };
 __device__ __forceinline__ void pf_enter(const TcArgs& a, TcPf& f) {
   if (f.cg >= a.n_chunks) return;
@@ -372,12 +374,18 @@ __device__ __forceinline__ void pf_enter(const TcArgs& a, TcPf& f) {
   f.j = 0;
   f.trow = (int32_t)fdiv((uint32_t)tt0, a.dtpr);
   f.tcol = tt0 - f.trow * a.tpr;
+  f.dband = a.dmain + tt0 / 15;  // (donor tiles only; once per chunk)
+  f.dchunk = tt0 % 15;
 }
 __device__ __forceinline__ void pf_next(const TcArgs& a, TcPf& f) {
   if (++f.j < f.n) {
     if (++f.tcol == a.tpr) {
       f.tcol = 0;
       ++f.trow;
+    }
+    if (++f.dchunk == 15) {
+      f.dchunk = 0;
+      ++f.dband;
     }
   } else {
     f.cg += gridDim.x;
@@ -394,12 +402,20 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// CW = 15 is the donor tiling of 15-chunk rows (1920-byte planes, config 4's chroma): main tile
+// b < dmain is band b's 15 chunk-bands (one box of the main map) plus one chunk-band of a donor
+// band (a 1-chunk box of the donor map into the tile's 16th KB); donors are the last
+// ceil(bands / 16) bands, taken in order, and what is left of them (at most 15 chunk-bands, all
+// in the last band) is one more tile, its 16th KB a fully out-of-bounds box (zero fill).  So a
+// 1920 x 1080 plane is 127 tiles instead of 135 with a 1/16 zero fill each.
 template <class MP, int R, int CW>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    fused_u8_tc_kernel(const __grid_constant__ CUtensorMap tmap, TcArgs a, DevMat dm, double* __restrict__ partial) {
+    fused_u8_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_d, TcArgs a,
+                       DevMat dm, double* __restrict__ partial) {
   using S = TcShape<R>;
   constexpr int N = S::N, NB = S::NB;
-  constexpr int BH = 16 / CW;  // bands per tile
+  constexpr bool DON = CW == 15;
+  constexpr int BH = DON ? 1 : 16 / CW;  // bands per tile
   // kind::i8: D s32 (2 << 4), A u8 (0 << 7), B s8 (1 << 10), both K-major, N >> 3, M >> 4
   // each tile is two MMA sets of N = NB (half h: block 2p + h of every pair), each into its own
   // TMEM half-stage, so an epilogue warp releases block 2p's columns before it computes
@@ -494,8 +510,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + slot * 8),
                      "r"((uint32_t)kTcTileBytes)
                      : "memory");
-        tma_load_5d(ring0 + slot * kTcTileBytes, &tmap, 0, 0, pf.trow * BH, pf.tcol * CW, (int32_t)pf.img,
-                    full0 + slot * 8);
+        if constexpr (DON) {
+          const bool main = pf.trow < a.dmain;
+          tma_load_5d(ring0 + slot * kTcTileBytes, &tmap, 0, 0, main ? pf.trow : a.dlast, main ? 0 : a.dc0,
+                      (int32_t)pf.img, full0 + slot * 8);
+          tma_load_5d(ring0 + slot * kTcTileBytes + 15 * 1024, &tmap_d, 0, 0, main ? pf.dband : 0,
+                      main ? pf.dchunk : 15, (int32_t)pf.img, full0 + slot * 8);
+        } else {
+          tma_load_5d(ring0 + slot * kTcTileBytes, &tmap, 0, 0, pf.trow * BH, pf.tcol * CW, (int32_t)pf.img,
+                      full0 + slot * 8);
+        }
       }
       __syncwarp();
       pf_next(a, pf);
@@ -617,7 +641,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 template <class MP, int R, int CW>
-bool launch_tc_rc(const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial, cudaStream_t st) {
+bool launch_tc_rc(const CUtensorMap& map, const CUtensorMap& map_d, const TcArgs& a, const DevMat& dm, double* partial,
+                  cudaStream_t st) {
   // the shared-memory opt-in is a per-device function attribute: set it once per device
   static std::mutex mu;
   static int8_t state[kMaxDevices] = {};
@@ -627,19 +652,20 @@ bool launch_tc_rc(const CUtensorMap& map, const TcArgs& a, const DevMat& dm, dou
       }))
     return false;
   const int64_t grid = (int64_t)a.n_chunks < sms_s() ? (int64_t)a.n_chunks : sms_s();
-  if (launch_pdl(fused_u8_tc_kernel<MP, R, CW>, dim3((unsigned)grid), dim3(kTcThreads), kTcSmem, st, map, a, dm,
-                 partial) != cudaSuccess)
+  if (launch_pdl(fused_u8_tc_kernel<MP, R, CW>, dim3((unsigned)grid), dim3(kTcThreads), kTcSmem, st, map, map_d, a,
+                 dm, partial) != cudaSuccess)
     return false;
   return true;
 }
 
 template <class MP, int R>
-bool launch_tc_r(int cw, const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial,
-                 cudaStream_t st) {
+bool launch_tc_r(int cw, const CUtensorMap& map, const CUtensorMap& map_d, const TcArgs& a, const DevMat& dm,
+                 double* partial, cudaStream_t st) {
   switch (cw) {
-    case 2: return launch_tc_rc<MP, R, 2>(map, a, dm, partial, st);
-    case 1: return launch_tc_rc<MP, R, 1>(map, a, dm, partial, st);
-    case 16: return launch_tc_rc<MP, R, 16>(map, a, dm, partial, st);
+    case 2: return launch_tc_rc<MP, R, 2>(map, map_d, a, dm, partial, st);
+    case 1: return launch_tc_rc<MP, R, 1>(map, map_d, a, dm, partial, st);
+    case 16: return launch_tc_rc<MP, R, 16>(map, map_d, a, dm, partial, st);
+    case 15: return launch_tc_rc<MP, R, 15>(map, map_d, a, dm, partial, st);
     default: return false;
   }
 }
@@ -647,29 +673,30 @@ bool launch_tc_r(int cw, const CUtensorMap& map, const TcArgs& a, const DevMat& 
 // compiled (matrix, r) pairs: T1 at config 4's r = 10 and the Lena figures' r = 3, 14
 // (P:L2380-2444); runtime integer matrices at r = 10
 template <class MP>
-bool launch_tc(int r, int cw, const CUtensorMap& map, const TcArgs& a, const DevMat& dm, double* partial,
-               cudaStream_t st) {
+bool launch_tc(int r, int cw, const CUtensorMap& map, const CUtensorMap& map_d, const TcArgs& a, const DevMat& dm,
+               double* partial, cudaStream_t st) {
   if constexpr (!MP::kConst) {
-    return r == 10 && launch_tc_r<MP, 10>(cw, map, a, dm, partial, st);
+    return r == 10 && launch_tc_r<MP, 10>(cw, map, map_d, a, dm, partial, st);
   } else {
     switch (r) {
-      case 3: return launch_tc_r<MP, 3>(cw, map, a, dm, partial, st);
-      case 10: return launch_tc_r<MP, 10>(cw, map, a, dm, partial, st);
-      case 14: return launch_tc_r<MP, 14>(cw, map, a, dm, partial, st);
+      case 3: return launch_tc_r<MP, 3>(cw, map, map_d, a, dm, partial, st);
+      case 10: return launch_tc_r<MP, 10>(cw, map, map_d, a, dm, partial, st);
+      case 14: return launch_tc_r<MP, 14>(cw, map, map_d, a, dm, partial, st);
       default: return false;
     }
   }
 }
 
-// 5-D map {128 B, 8 rows, bands, chunks, images}, strides {row, 8 rows, 128 B, image}
-bool make_tc_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int cw) {
+// 5-D map {128 B, 8 rows, bands, chunks, images}, strides {row, 8 rows, 128 B, image}; box of
+// bh bands x cw chunks
+bool make_tc_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int bh, int cw) {
   auto enc = tmap_encoder();
   if (!enc) return false;
   const int64_t istride = g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride;
   const cuuint64_t dims[5] = {128, 8, (cuuint64_t)(g.height / 8), (cuuint64_t)(g.width / 128),
                               (cuuint64_t)g.n_images};
   const cuuint64_t strides[4] = {(cuuint64_t)g.row_stride, (cuuint64_t)(8 * g.row_stride), 128, (cuuint64_t)istride};
-  const cuuint32_t box[5] = {128, 8, (cuuint32_t)(16 / cw), (cuuint32_t)cw, 1};
+  const cuuint32_t box[5] = {128, 8, (cuuint32_t)bh, (cuuint32_t)cw, 1};
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(src), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -679,27 +706,46 @@ bool make_tc_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int 
 }  // namespace
 
 // tile shape of the tensor-core kernel: CW 128-byte chunks x 16/CW bands, the CW in {2, 16, 1}
-// with the fewest tiles (zero-filled parts of edge tiles cost MMA rows, never HBM bytes)
+// with the fewest tiles (zero-filled parts of edge tiles cost MMA rows, never HBM bytes), or the
+// donor tiling (CW = 15) of 15-chunk rows
 TcPlan tc_plan(const adct_geom& g) {
   TcPlan p{};
   if (g.width <= 0 || g.height <= 0 || (g.width % 128) != 0) return p;  // whole 128-byte chunks only
   const int64_t nch = g.width / 128, nbd = g.height / 8;
   int64_t best = -1;
-  static const int force_cw = [] {  // A/B hook: ADCT_TC_CW=1|2|16 forces the tile shape
+  static const int force_cw = [] {  // A/B hook: ADCT_TC_CW=1|2|16|15 forces the tile shape
     const char* e = std::getenv("ADCT_TC_CW");
     return e ? std::atoi(e) : 0;
   }();
-  for (int cw : {2, 16, 1}) {
+  for (int cw : {2, 16, 1, 15}) {
     if (force_cw && cw != force_cw) continue;
-    const int64_t bh = 16 / cw;
-    const int64_t tiles = ((nch + cw - 1) / cw) * ((nbd + bh - 1) / bh);
+    int64_t tiles;
+    if (cw == 15) {
+      static const bool no_donor = std::getenv("ADCT_TC_NODONOR") != nullptr;  // A/B hook
+      if (nch != 15 || no_donor) continue;
+      const int64_t d = (nbd + 15) / 16;  // donor bands
+      tiles = (nbd - d) + ((16 * d - nbd) > 0 ? 1 : 0);
+    } else {
+      const int64_t bh = 16 / cw;
+      tiles = ((nch + cw - 1) / cw) * ((nbd + bh - 1) / bh);
+    }
     if (best < 0 || tiles < best) {
       best = tiles;
       p.cw = cw;
     }
   }
-  p.tpr = (int32_t)((nch + p.cw - 1) / p.cw);
-  p.tpi = (int32_t)(p.tpr * ((nbd + 16 / p.cw - 1) / (16 / p.cw)));
+  if (p.cw == 0) return p;
+  if (p.cw == 15) {
+    const int64_t d = (nbd + 15) / 16;
+    p.dmain = (int32_t)(nbd - d);
+    p.dlast = (int32_t)(nbd - 1);
+    p.dc0 = (int32_t)(p.dmain - 15 * (d - 1));
+    p.tpr = 1;
+    p.tpi = (int32_t)best;
+  } else {
+    p.tpr = (int32_t)((nch + p.cw - 1) / p.cw);
+    p.tpi = (int32_t)(p.tpr * ((nbd + 16 / p.cw - 1) / (16 / p.cw)));
+  }
   p.ct = tc_chunk_tiles(p.tpi);
   p.cpi = (p.tpi + p.ct - 1) / p.ct;
   p.n_chunks = g.n_images * (int64_t)p.cpi;
@@ -715,8 +761,13 @@ bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, i
                  double* partial, cudaStream_t st, adct_status* status) {
   const TcPlan p = tc_plan(g);
   if (!p.ok || g.n_images == 0 || !aligned(src, 16) || !m->is_int) return false;
-  CUtensorMap map;
-  if (!make_tc_tmap(&map, src, g, p.cw)) return false;
+  CUtensorMap map, map_d;
+  if (p.cw == 15) {
+    if (!make_tc_tmap(&map, src, g, 1, 15) || !make_tc_tmap(&map_d, src, g, 1, 1)) return false;
+  } else {
+    if (!make_tc_tmap(&map, src, g, 16 / p.cw, p.cw)) return false;
+    map_d = map;
+  }
   TcArgs a;
   a.tpr = p.tpr;
   a.tpi = p.tpi;
@@ -725,8 +776,11 @@ bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, i
   a.n_chunks = (uint32_t)p.n_chunks;
   a.dcpi = make_fastdiv((uint32_t)p.cpi);
   a.dtpr = make_fastdiv((uint32_t)p.tpr);
-  const bool ok = m->specialized ? launch_tc<T1Mat>(r, p.cw, map, a, m->dev, partial, st)
-                                 : launch_tc<RtMat>(r, p.cw, map, a, m->dev, partial, st);
+  a.dmain = p.dmain;
+  a.dlast = p.dlast;
+  a.dc0 = p.dc0;
+  const bool ok = m->specialized ? launch_tc<T1Mat>(r, p.cw, map, map_d, a, m->dev, partial, st)
+                                 : launch_tc<RtMat>(r, p.cw, map, map_d, a, m->dev, partial, st);
   if (!ok) return false;
   count_launch();
   if ((*status = launch_status()) != ADCT_OK) return true;

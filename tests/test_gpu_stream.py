@@ -126,7 +126,7 @@ _VARIANT_SCRIPT = textwrap.dedent("""
 
 
 @pytest.mark.parametrize("env", [{}, {"ADCT_DISABLE_STREAM": "1"}, {"ADCT_HOT": "simt"}, {"ADCT_TC_CW": "1"},
-                                 {"ADCT_TC_CW": "16"}])
+                                 {"ADCT_TC_CW": "16"}, {"ADCT_TC_CW": "15"}])
 def test_kernel_variants_agree_with_oracle(tmp_path, env):
     """Every kernel variant on the same geometries: the tensor-core kernel with its automatic tile
     shape and with forced 1- and 16-chunk-wide tiles; the SIMT streaming kernel; the generic fused
@@ -143,6 +143,37 @@ def test_kernel_variants_agree_with_oracle(tmp_path, env):
         img = synth.ar1_field(n, h, w, 0.95, seed=h + w)
         ref.append(oracle.codec_sse(img.numpy(), [10], t=M.T1).ravel())
     _check(got, np.concatenate(ref))
+
+
+# --- donor tiling of 15-chunk rows (1920-byte planes: config 4's chroma, tc.cu CW = 15) ----------
+# bands = H / 8 across the cases the plan distinguishes: fewer than 16 (no main tile, only the
+# leftover), exactly 16 (no leftover), 17 / 31 / 33 (a leftover of 15 / 1 / 15 chunk-bands), 135
+DONOR_GEOMS = [(3, 8, 1920), (2, 120, 1920), (2, 128, 1920), (2, 136, 1920), (2, 248, 1920), (1, 264, 1920),
+               (3, 1080, 1920)]
+
+
+@pytest.mark.parametrize("geom", DONOR_GEOMS)
+def test_donor_tiles(mats, geom):
+    """Main tiles (one band + one donor chunk-band), the leftover tile (the last band's tail, its
+    16th KB a fully out-of-bounds box) and the per-image sums over them equal the oracle for T1
+    at r = 3, 10, 14 and a runtime matrix at r = 10."""
+    n, h, w = geom
+    img = synth.ar1_field(n, h, w, 0.95, seed=h + 3 * n)
+    for name, r in (("T1", 3), ("T1", 10), ("T1", 14), ("T2", 10)):
+        sse = adct.approx_dct8x8_fused_sse(mats[name], img.to(DEV), [r]).cpu().numpy()
+        _check(sse, oracle.codec_sse(img.numpy(), [r], t=np.array(catalog.INTEGER[name]).reshape(8, 8)))
+
+
+def test_donor_tiles_padded_strides(mats):
+    """Donor boxes through padded row / image strides: the 15-chunk map's out-of-bounds chunk is
+    the 16th 128-byte chunk of the WIDTH, never the row padding."""
+    img = synth.ar1_field(2, 136, 1920, 0.9, seed=9)
+    big = torch.full((2, 144, 2048), 255, dtype=torch.uint8)
+    big[:, :136, :1920] = img
+    view = big.to(DEV)[:, :136, :1920]
+    assert view.stride() == (144 * 2048, 2048, 1)
+    sse = adct.approx_dct8x8_fused_sse(mats["T1"], view, [10]).cpu().numpy()
+    _check(sse, oracle.codec_sse(img.numpy(), [10], t=M.T1))
 
 
 # --- several planes in one launch (approx_dct8x8_fused_sse_planes; the Y, U, V planes of C4) ------
