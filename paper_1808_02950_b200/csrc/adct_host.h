@@ -249,6 +249,10 @@ struct TcPlan {
   bool ok;
 };
 TcPlan tc_plan(const adct_geom& g);  // tc.cu
+// the tensor-core path for one plane (tc.cu); false when it does not cover the call
+bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
+                 double* partial, cudaStream_t st, adct_status* status, int64_t split = 0, double* sse2 = nullptr,
+                 double* psnr2 = nullptr);
 
 inline int64_t stream_partials_per_image(const adct_geom& g) {
   int64_t best = 0;

@@ -405,8 +405,6 @@ bool launch_wtile(int r, int tw, const CUtensorMap& map, const WtArgs& a, const 
 // The streaming path for (u8 source, integer matrix, no clip, one r); returns false when the
 // geometry or r is not covered (the caller then uses the generic fused kernels).
 // On success the per-image SSE is in sse[n_images] (finalize launched on st).
-bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
-                 double* partial, cudaStream_t st, adct_status* status);
 
 // ADCT_HOT=simt selects this file's SIMT streaming kernel instead of the tensor-core one (tc.cu;
 // A/B runs and the SIMT parity tests)

@@ -757,8 +757,10 @@ TcPlan tc_plan(const adct_geom& g) {
 
 // The tensor-core streaming path for (u8 source, integer matrix, no clip, one r); false when
 // the geometry or r is not covered (the caller then uses the SIMT streaming kernel).
+// split > 0: the images are two planes of one geometry stacked in memory (see fused_u8_tc_planes);
+// images [0, split) finalize into sse/psnr, the rest into sse2/psnr2
 bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
-                 double* partial, cudaStream_t st, adct_status* status) {
+                 double* partial, cudaStream_t st, adct_status* status, int64_t split, double* sse2, double* psnr2) {
   const TcPlan p = tc_plan(g);
   if (!p.ok || g.n_images == 0 || !aligned(src, 16) || !m->is_int) return false;
   CUtensorMap map, map_d;
@@ -786,14 +788,23 @@ bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, i
   if ((*status = launch_status()) != ADCT_OK) return true;
   SlotMap sm{};
   sm.s[0] = 0;
-  launch_finalize(partial, p.cpi * kTcPartials, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0, sse, psnr,
-                  st);
+  const int32_t ppi = p.cpi * kTcPartials;  // partials per image
+  if (split > 0) {
+    launch_finalize(partial, ppi, split, 1, sm, 1, (double)g.height * g.width, 255.0, sse, psnr, st);
+    launch_finalize(partial + split * ppi, ppi, g.n_images - split, 1, sm, 1, (double)g.height * g.width, 255.0,
+                    sse2, psnr2, st);
+  } else {
+    launch_finalize(partial, ppi, g.n_images, 1, sm, 1, (double)g.height * g.width, 255.0, sse, psnr, st);
+  }
   *status = launch_status();
   return true;
 }
 
 // Several planes (the Y, U, V planes of config 4) on the tensor-core path: all of them or none
-// (false, nothing launched), one launch per plane on the stream.  A single launch over the
+// (false, nothing launched), one launch per plane on the stream -- except that two consecutive
+// planes of the same geometry that lie back to back in memory (plane i + 1 starts where plane i's
+// last image ends, as the U and V stacks of bench.py do) run as ONE launch over both image ranges:
+// one ramp and one tail instead of two, per-image sums bit-identical (chunks follow the geometry).  A single launch over the
 // concatenated chunk lists of the planes (runtime tile shape, plane table) was built and measured:
 // it removed two ramps and tails but its epilogue compiled to a different schedule that ran the
 // luma plane 3-10 % slower and under the power cap (1.49-1.50 ms vs 1.46 ms per C4 step, same box;
@@ -808,7 +819,31 @@ bool fused_u8_tc_planes(const adct_matrix* m, int n, const uint8_t* const* src, 
     const TcPlan p = tc_plan(g[i]);
     if (!p.ok || g[i].n_images == 0 || !aligned(src[i], 16)) return false;
   }
+  static const bool no_merge = std::getenv("ADCT_TC_NOMERGE") != nullptr;  // A/B hook
   for (int i = 0; i < n; ++i) {
+    const int64_t is0 = g[i].n_images > 1 ? g[i].image_stride : (int64_t)g[i].height * g[i].row_stride;
+    bool merge = !no_merge && i + 1 < n;
+    if (merge) {
+      const adct_geom& h = g[i + 1];
+      const int64_t is1 = h.n_images > 1 ? h.image_stride : (int64_t)h.height * h.row_stride;
+      adct_geom gm = g[i];
+      gm.n_images = g[i].n_images + h.n_images;
+      gm.image_stride = is0;
+      const TcPlan pm = tc_plan(gm);
+      const int64_t need = g[i].n_images * (int64_t)pm.cpi * kTcPartials;  // plane i's partials, merged plan
+      merge = h.width == g[i].width && h.height == g[i].height && h.row_stride == g[i].row_stride && is1 == is0 &&
+              src[i + 1] == src[i] + g[i].n_images * is0 && pm.ok && partial[i + 1] >= partial[i] + need;
+      if (merge) {
+        if (!fused_u8_tc(m, src[i], gm, r, sse[i], psnr ? psnr[i] : nullptr, partial[i], st, status, g[i].n_images,
+                         sse[i + 1], psnr ? psnr[i + 1] : nullptr)) {
+          *status = ADCT_E_CUDA;
+          return true;
+        }
+        if (*status != ADCT_OK) return true;
+        ++i;
+        continue;
+      }
+    }
     if (!fused_u8_tc(m, src[i], g[i], r, sse[i], psnr ? psnr[i] : nullptr, partial[i], st, status)) {
       *status = ADCT_E_CUDA;  // a plane that passed the checks failed to launch
       return true;

@@ -202,6 +202,42 @@ def test_planes_equal_per_plane_calls(mats, shapes):
             assert np.all(np.abs(s.cpu().numpy() - ref) <= 1e-5 * ref)
 
 
+@pytest.mark.parametrize("counts,h,w", [((3, 3), 1080, 1920), ((2, 5), 136, 384), ((1, 1), 64, 1920),
+                                        ((4, 2), 40, 1280)])
+def test_planes_back_to_back_one_launch(mats, counts, h, w):
+    """Two planes of one geometry stored back to back (plane 2 starts where plane 1's last image
+    ends: bench.py's U and V) run as ONE launch over both image ranges; SSE and PSNR equal the
+    per-plane calls bit for bit (chunks follow the geometry), and one launch fewer is counted."""
+    na, nb = counts
+    both = synth.ar1_field(na + nb, h, w, 0.9, seed=na * 10 + nb).to(DEV)
+    a, b = both[:na], both[na:]
+    y = synth.ar1_field(2, 2 * h, 2 * w, 0.95, seed=1).to(DEV)
+    for planes in ([a, b], [y, a, b]):
+        n0 = adct.launch_count()
+        sse, psnr = adct.approx_dct8x8_fused_sse_planes(mats["T1"], planes, 10)
+        torch.cuda.synchronize()
+        merged = adct.launch_count() - n0
+        n0 = adct.launch_count()
+        for p, s, q in zip(planes, sse, psnr):
+            s1, q1 = adct.approx_dct8x8_fused_sse(mats["T1"], p, [10], return_psnr=True)
+            assert torch.equal(s, s1[:, 0]) and torch.equal(q, q1[:, 0])
+        torch.cuda.synchronize()
+        assert merged == adct.launch_count() - n0 - 1  # one hot-kernel launch fewer (the finalizes stay per plane)
+    ref = oracle.codec_sse(both.cpu().numpy(), [10], t=M.T1)[:, 0]
+    sse, _ = adct.approx_dct8x8_fused_sse_planes(mats["T1"], [a, b], 10)
+    _check(torch.cat(sse).cpu().numpy(), ref)
+
+
+def test_planes_not_back_to_back(mats):
+    """Same geometry with a gap between the planes, or a different row stride: separate launches,
+    same results as the per-plane calls."""
+    buf = synth.ar1_field(5, 136, 384, 0.9, seed=3).to(DEV)
+    a, b = buf[:2], buf[3:]  # one image gap
+    sse, psnr = adct.approx_dct8x8_fused_sse_planes(mats["T1"], [a, b], 10)
+    for p, s in zip((a, b), sse):
+        assert torch.equal(s, adct.approx_dct8x8_fused_sse(mats["T1"], p, [10])[:, 0])
+
+
 def test_planes_argument_errors(mats):
     y = torch.zeros((1, 64, 128), dtype=torch.uint8, device=DEV)
     with pytest.raises(ValueError):
