@@ -30,6 +30,12 @@
 #ifndef ADCT_Q_PACKED
 #define ADCT_Q_PACKED 0
 #endif
+// ADCT_Q_FAST: the C3 quantiser with a directed-rounding FMA at the rational positions (exact by
+// construction, no remainder correction) and a fused remainder at the irrational ones; 0 = the
+// round-2 remainder-corrected form (A/B)
+#ifndef ADCT_Q_FAST
+#define ADCT_Q_FAST 1
+#endif
 
 namespace adct {
 namespace {
@@ -211,8 +217,16 @@ bool enc2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, uint64_t inner,
 // and the exact rounding remainder d = v - round(v) (Fast2Sum) flags coefficients within 2^-14
 // of a rounding boundary — every exact tie included — for which the block takes the exact
 // integer rule (2m-1)^2 P <= 4 Y^2 < (2m+1)^2 P, P = step^2 n_k n_l (fp64, exact below 2^53).
+//
+// ADCT_Q_FAST (default): at the 40 rational positions c is an even integer and
+// |q| = floor(A / c), A = |Y| + c/2 an integer < 2^23.  With u = fp32 1/c rounded UP, the exact
+// product A u lies in [A/c, A/c + A 2^-23 / c): at a multiple A = m c it is >= m, otherwise
+// A/c <= m - 1/c and A 2^-23 < 1 keeps it below m, so floor(A u) = floor(A / c) for every such A
+// (tests/test_kernel_arith.py checks every A).  One FFMA rounding toward -inf onto 1.5 * 2^23
+// gives 1.5 * 2^23 + |q|; 3 * 2^23 minus that is 1.5 * 2^23 - |q|, whose low 16 bits are -|q|.
 struct QTab {
   float inv[64];    // fp32(1 / c_kl)
+  float invu[64];   // fp32(1 / c_kl) rounded up (rational positions; ADCT_Q_FAST)
   double p[64];     // P_kl = step^2 n_k n_l
 };
 
@@ -392,6 +406,11 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
             const float yy = y[k][l + e] - (kl == 0 ? 64.0f * 32768.0f : 0.0f);  // exact
             y[k][l + e] = yy;
             if (t1_rational(k, l + e)) {
+#if ADCT_Q_FAST
+              const float A = fabsf(yy) + stepf * (0.5f * (float)t1_sqrt_nn(k, l + e));  // exact
+              const float up = __fmaf_rd(A, qt.invu[kl], 12582912.0f);                  // 1.5*2^23 + |q|
+              u[e] = __float_as_uint(yy < 0.0f ? 25165824.0f - up : up);
+#else
               // |q| = floor((|Y| + c/2) / c): estimate, then the exact remainder decides
               const float c = stepf * (float)t1_sqrt_nn(k, l + e);
               const float A = fabsf(yy) + 0.5f * c;
@@ -401,10 +420,17 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
               const float mf = rem < 0.0f ? m0 - 1.0f : m0;
               const float qf = __uint_as_float(__float_as_uint(mf) | (__float_as_uint(yy) & 0x80000000u));
               u[e] = __float_as_uint(qf + 12582912.0f);
+#endif
             } else {
+#if ADCT_Q_FAST
+              // nearest integer of Y/c (one rounding), and the remainder Y/c - that in one FFMA
+              const float f = fmaf(yy, qt.inv[kl], 12582912.0f);
+              near |= fabsf(fmaf(yy, qt.inv[kl], 12582912.0f - f)) > 0.49993896f;  // within 2^-14 of a boundary
+#else
               const float v = yy * qt.inv[kl];
               const float f = v + 12582912.0f;
               near |= fabsf(v - (f - 12582912.0f)) > 0.49993896f;  // within 2^-14 of a boundary
+#endif
               u[e] = __float_as_uint(f);
             }
           }
@@ -416,9 +442,14 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
         for (int kl = 0; kl < 64; ++kl) {
           if (t1_rational(kl >> 3, kl & 7)) continue;
           const float yy = y[kl >> 3][kl & 7];
+#if ADCT_Q_FAST
+          const float f = fmaf(yy, qt.inv[kl], 12582912.0f);
+          if (near && fabsf(fmaf(yy, qt.inv[kl], 12582912.0f - f)) > 0.49993896f) {
+#else
           const float v = yy * qt.inv[kl];
           const float f = v + 12582912.0f;
           if (near && fabsf(v - (f - 12582912.0f)) > 0.49993896f) {
+#endif
             const double a2 = 4.0 * (double)yy * (double)yy, pp = qt.p[kl];
             double mm = rint(fabs((double)yy) / sqrt(pp));
             if (mm >= 1.0 && (2.0 * mm - 1.0) * (2.0 * mm - 1.0) * pp > a2) mm -= 1.0;
@@ -547,6 +578,13 @@ bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g,
       const double p = (double)step * step * (double)m->n[k] * (double)m->n[l];
       qt.p[k * 8 + l] = p;
       qt.inv[k * 8 + l] = (float)(1.0 / std::sqrt(p));
+      qt.invu[k * 8 + l] = 0.0f;
+      if (t1_rational(k, l)) {  // c = step sqrt(n_k n_l), an integer: fp32 1/c rounded up
+        const double c = (double)step * t1_sqrt_nn(k, l);
+        float u = (float)(1.0 / c);
+        if ((double)u * c < 1.0) u = std::nextafter(u, 1.0f);  // exact product: 24 + 17 bits
+        qt.invu[k * 8 + l] = u;
+      }
     }
   const int32_t bh = g.height / 8;
   const float stepf = (float)step;

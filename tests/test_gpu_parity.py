@@ -343,6 +343,16 @@ def test_quantiser_extreme_and_uniform(mats):
         assert np.array_equal(q, oracle.quantize(oracle.forward_int(M.T1, img.numpy()), n, 16))
 
 
+@pytest.mark.parametrize("step", [1, 3, 7, 17, 100, 255, 4096])
+def test_quantiser_other_steps(mats, step):
+    """Steps other than 16 (the TMA kernel accepts 1..4096; its directed-rounding FMA at the
+    rational positions is exact for every A < 2^23, tests/test_kernel_arith.py): bit-exact."""
+    n, _ = oracle.row_scaling(M.T1)
+    for img in (images("uniform", 2, 128, 256, seed=44), images("extreme", 2, 128, 256, seed=45)):
+        q = adct.approx_dct8x8_fwd_quant(mats["T1"], img.to(DEV), step).cpu().numpy()
+        assert np.array_equal(q, oracle.quantize(oracle.forward_int(M.T1, img.numpy()), n, step))
+
+
 def _tie_blocks(seed=43):
     """u8 blocks that put EVERY reachable exact tie Y = (m + 1/2) * 16 sqrt(n_k n_l) of T1 at each
     of the 40 positions where sqrt(n_k n_l) is rational (reading A10; S_1).  Y_kl =
