@@ -228,7 +228,16 @@ struct QTab {
   float inv[64];    // fp32(1 / c_kl)
   float invu[64];   // fp32(1 / c_kl) rounded up (rational positions; ADCT_Q_FAST)
   double p[64];     // P_kl = step^2 n_k n_l
+  double rsp[64];   // 1 / sqrt(P_kl) (fp64; the exact rule's estimate, corrected by the integer tests)
+  float ru[4];      // invu by sqrt(n_k n_l) = 8, 12, 18, 20 (ADCT_Q_FAST: 6 registers, not 64 loads)
+  float ri[2];      // inv at the irrational positions, n_k n_l = 160, 360
 };
+__host__ __device__ constexpr int q_rclass(int k, int l) {  // index of sqrt(n_k n_l) in {8, 12, 18, 20}
+  return ((k & 3) == 2) ? 3 : (((k & 1) + (l & 1)) == 0 ? 0 : (((k & 1) + (l & 1)) == 1 ? 1 : 2));
+}
+__host__ __device__ constexpr int q_iclass(int k, int l) {  // 0: n_k n_l = 160, 1: 360
+  return ((k & 1) | (l & 1));
+}
 
 constexpr int kQWarps = 12;                 // 16 KB of shared memory per warp
 constexpr int kQInSlots = 2;
@@ -285,6 +294,10 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
     if (pt < n_tiles) issue(s);
   const uint32_t grp = (uint32_t)(lane / BPR), pos = (uint32_t)(lane % BPR);
   const uint32_t lane_in = (uint32_t)pos * 8u + grp * 16u * TW;
+#if ADCT_Q_FAST
+  const float qru[4] = {qt.ru[0], qt.ru[1], qt.ru[2], qt.ru[3]};
+  const float qri[2] = {qt.ri[0], qt.ri[1]};
+#endif
   int slot = 0;
   uint32_t phase = 0;
   for (uint32_t t = wid; t < n_tiles; t += nw) {
@@ -408,7 +421,7 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
             if (t1_rational(k, l + e)) {
 #if ADCT_Q_FAST
               const float A = fabsf(yy) + stepf * (0.5f * (float)t1_sqrt_nn(k, l + e));  // exact
-              const float up = __fmaf_rd(A, qt.invu[kl], 12582912.0f);                  // 1.5*2^23 + |q|
+              const float up = __fmaf_rd(A, qru[q_rclass(k, l + e)], 12582912.0f);      // 1.5*2^23 + |q|
               u[e] = __float_as_uint(yy < 0.0f ? 25165824.0f - up : up);
 #else
               // |q| = floor((|Y| + c/2) / c): estimate, then the exact remainder decides
@@ -424,8 +437,9 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
             } else {
 #if ADCT_Q_FAST
               // nearest integer of Y/c (one rounding), and the remainder Y/c - that in one FFMA
-              const float f = fmaf(yy, qt.inv[kl], 12582912.0f);
-              near |= fabsf(fmaf(yy, qt.inv[kl], 12582912.0f - f)) > 0.49993896f;  // within 2^-14 of a boundary
+              const float iv = qri[q_iclass(k, l + e)];
+              const float f = fmaf(yy, iv, 12582912.0f);
+              near |= fabsf(fmaf(yy, iv, 12582912.0f - f)) > 0.49993896f;  // within 2^-14 of a boundary
 #else
               const float v = yy * qt.inv[kl];
               const float f = v + 12582912.0f;
@@ -451,7 +465,7 @@ __global__ void __launch_bounds__(32 * kQWarps, 1)
           if (near && fabsf(v - (f - 12582912.0f)) > 0.49993896f) {
 #endif
             const double a2 = 4.0 * (double)yy * (double)yy, pp = qt.p[kl];
-            double mm = rint(fabs((double)yy) / sqrt(pp));
+            double mm = rint(fabs((double)yy) * qt.rsp[kl]);  // within 1 of the answer
             if (mm >= 1.0 && (2.0 * mm - 1.0) * (2.0 * mm - 1.0) * pp > a2) mm -= 1.0;
             else if ((2.0 * mm + 1.0) * (2.0 * mm + 1.0) * pp <= a2) mm += 1.0;
             const uint32_t q16 = (uint32_t)(uint16_t)(int16_t)(yy < 0.0f ? -(int)mm : (int)mm);
@@ -577,6 +591,7 @@ bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g,
     for (int l = 0; l < 8; ++l) {
       const double p = (double)step * step * (double)m->n[k] * (double)m->n[l];
       qt.p[k * 8 + l] = p;
+      qt.rsp[k * 8 + l] = 1.0 / std::sqrt(p);
       qt.inv[k * 8 + l] = (float)(1.0 / std::sqrt(p));
       qt.invu[k * 8 + l] = 0.0f;
       if (t1_rational(k, l)) {  // c = step sqrt(n_k n_l), an integer: fp32 1/c rounded up
@@ -586,6 +601,12 @@ bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g,
         qt.invu[k * 8 + l] = u;
       }
     }
+  for (int j = 0; j < 4; ++j) {  // the same values by class
+    static constexpr int kk[4] = {0, 0, 1, 2}, ll[4] = {0, 1, 1, 2};
+    qt.ru[j] = qt.invu[kk[j] * 8 + ll[j]];
+  }
+  qt.ri[0] = qt.inv[2 * 8 + 0];  // n = 20 x 8
+  qt.ri[1] = qt.inv[2 * 8 + 1];  // n = 20 x 18
   const int32_t bh = g.height / 8;
   const float stepf = (float)step;
   adct_status s = tw == 128 ? launch_quant<128>(tin, tout, qt, stepf, tpb, tpi, bh, (uint32_t)n_tiles, st)
