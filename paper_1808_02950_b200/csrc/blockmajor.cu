@@ -570,8 +570,21 @@ bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g,
                                    (cuuint64_t)(g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride)};
     const cuuint32_t box[3] = {(cuuint32_t)tw, (cuuint32_t)rows, 1};
     const cuuint32_t es[3] = {1, 1, 1};
+    static const int promo_env = [] {  // A/B hook: ADCT_Q_L2PROMO=0|64|128|256
+      const char* e = std::getenv("ADCT_Q_L2PROMO");
+      return e ? std::atoi(e) : -1;
+    }();
+    // a 128-byte-wide box with 256-byte promotion pulls the neighbouring 128 B of every row into L2;
+    // on 1920-byte rows (15 x 128 B) the granules straddle row ends and tiles of other warps, and
+    // part of that is evicted before its tile comes: ncu measured 2.41 GB read for 2.12 GB of
+    // pixels (config 3), 2.12 GB with 128-byte promotion, 1.160 -> 1.125 ms
+    const int promo = promo_env >= 0 ? promo_env : (tw == 128 ? 128 : 256);
+    const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                      : promo == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                      : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     if (enc(&tin, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(src), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }
