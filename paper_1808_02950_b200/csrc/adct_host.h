@@ -254,6 +254,10 @@ bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, i
                  double* partial, cudaStream_t st, adct_status* status, int64_t split = 0, double* sse2 = nullptr,
                  double* psnr2 = nullptr);
 
+// the tensor-core path of approx_dct8x8_fwd_quant (tc.cu); false when it does not cover the call
+bool fwd_quant_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t step, int16_t* q,
+                  cudaStream_t st, adct_status* status);
+
 inline int64_t stream_partials_per_image(const adct_geom& g) {
   int64_t best = 0;
   if (g.width % 128 == 0) {  // tensor-core tiles (any of its shapes)

@@ -19,6 +19,7 @@
 #include "adct_host.h"
 #include "tma.cuh"
 #include "packed.cuh"
+#include "quant.cuh"
 
 // ADCT_BM_PACKED: the round trip of the block-major kernel on column pairs with packed fp32
 // (packed.cuh); 0 = the scalar networks (A/B)
@@ -224,30 +225,8 @@ bool enc2d(CUtensorMap* map, CUtensorMapDataType dt, void* base, uint64_t inner,
 // A/c <= m - 1/c and A 2^-23 < 1 keeps it below m, so floor(A u) = floor(A / c) for every such A
 // (tests/test_kernel_arith.py checks every A).  One FFMA rounding toward -inf onto 1.5 * 2^23
 // gives 1.5 * 2^23 + |q|; 3 * 2^23 minus that is 1.5 * 2^23 - |q|, whose low 16 bits are -|q|.
-struct QTab {
-  float inv[64];    // fp32(1 / c_kl)
-  float invu[64];   // fp32(1 / c_kl) rounded up (rational positions; ADCT_Q_FAST)
-  double p[64];     // P_kl = step^2 n_k n_l
-  double rsp[64];   // 1 / sqrt(P_kl) (fp64; the exact rule's estimate, corrected by the integer tests)
-  float ru[4];      // invu by sqrt(n_k n_l) = 8, 12, 18, 20 (ADCT_Q_FAST: 6 registers, not 64 loads)
-  float ri[2];      // inv at the irrational positions, n_k n_l = 160, 360
-};
-__host__ __device__ constexpr int q_rclass(int k, int l) {  // index of sqrt(n_k n_l) in {8, 12, 18, 20}
-  return ((k & 3) == 2) ? 3 : (((k & 1) + (l & 1)) == 0 ? 0 : (((k & 1) + (l & 1)) == 1 ? 1 : 2));
-}
-__host__ __device__ constexpr int q_iclass(int k, int l) {  // 0: n_k n_l = 160, 1: 360
-  return ((k & 1) | (l & 1));
-}
-
 constexpr int kQWarps = 12;                 // 16 KB of shared memory per warp
 constexpr int kQInSlots = 2;
-
-__host__ __device__ constexpr bool t1_rational(int k, int l) {
-  return ((k & 3) == 2) == ((l & 3) == 2);
-}
-__host__ __device__ constexpr int t1_sqrt_nn(int k, int l) {  // sqrt(n_k n_l) where it is an integer
-  return ((k & 3) == 2) ? 20 : ((k & 3) == 0 ? ((l & 3) == 0 ? 8 : 12) : ((l & 3) == 0 ? 12 : 18));
-}
 
 template <int TW>
 __global__ void __launch_bounds__(32 * kQWarps, 1)
@@ -600,26 +579,7 @@ bool fwd_quant_tma(const adct_matrix* m, const uint8_t* src, const adct_geom& g,
       return false;
   }
   QTab qt;
-  for (int k = 0; k < 8; ++k)
-    for (int l = 0; l < 8; ++l) {
-      const double p = (double)step * step * (double)m->n[k] * (double)m->n[l];
-      qt.p[k * 8 + l] = p;
-      qt.rsp[k * 8 + l] = 1.0 / std::sqrt(p);
-      qt.inv[k * 8 + l] = (float)(1.0 / std::sqrt(p));
-      qt.invu[k * 8 + l] = 0.0f;
-      if (t1_rational(k, l)) {  // c = step sqrt(n_k n_l), an integer: fp32 1/c rounded up
-        const double c = (double)step * t1_sqrt_nn(k, l);
-        float u = (float)(1.0 / c);
-        if ((double)u * c < 1.0) u = std::nextafter(u, 1.0f);  // exact product: 24 + 17 bits
-        qt.invu[k * 8 + l] = u;
-      }
-    }
-  for (int j = 0; j < 4; ++j) {  // the same values by class
-    static constexpr int kk[4] = {0, 0, 1, 2}, ll[4] = {0, 1, 1, 2};
-    qt.ru[j] = qt.invu[kk[j] * 8 + ll[j]];
-  }
-  qt.ri[0] = qt.inv[2 * 8 + 0];  // n = 20 x 8
-  qt.ri[1] = qt.inv[2 * 8 + 1];  // n = 20 x 18
+  q_fill(qt, step, m->n);
   const int32_t bh = g.height / 8;
   const float stepf = (float)step;
   adct_status s = tw == 128 ? launch_quant<128>(tin, tout, qt, stepf, tpb, tpi, bh, (uint32_t)n_tiles, st)

@@ -422,6 +422,7 @@ adct_status approx_dct8x8_fwd_quant(const adct_matrix* m, const uint8_t* src, ad
   if (nb == 0) return ADCT_OK;
   if (!g_disable_stream) {  // TMA-streamed kernel (u8 tiles in, swizzled int16 tiles out)
     adct_status qs = ADCT_OK;
+    if (fwd_quant_tc(m, src, g, step, q, (cudaStream_t)stream, &qs)) return qs;  // tensor-core forward
     if (fwd_quant_tma(m, src, g, step, q, (cudaStream_t)stream, &qs)) return qs;
   }
   DevMat dm = m->dev;

@@ -15,6 +15,7 @@
 // (P:L2742-2770), and T(N)^T back up the column.  Pass 3: thread (b, i) applies T(N)^T to its row
 // and writes the reconstruction.  A row pitch of an odd number of 16-byte units (N + 4) keeps
 // the 128-bit row passes and the scalar column pass conflict-free.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -367,6 +368,216 @@ __global__ void __launch_bounds__(kJamNT, N == 16 ? ADCT_JAM_MINB16 : ADCT_JAM_M
   }
 }
 
+
+// ---- version 2: two rows / two columns per thread on packed fp32 ------------------------------
+// The networks run on float2 values whose halves are two INDEPENDENT vectors (two rows of a block
+// in passes 1 and 3, two adjacent columns in pass 2), so the recursion is the scalar one with
+// FADD2 / FFMA2 -- no lane swaps -- and every exchange through shared memory is a 128-bit access:
+// half the issued FP32 instructions and a third of the shared-memory instructions per sample of
+// the one-row-per-thread kernel above (which was bound by issue slots and the MIO queue).
+template <int N>
+struct Jam2 {
+  __device__ __forceinline__ static void fwd(const float2* x, float2* y) {
+    float2 u[N / 2], v[N / 2], yu[N / 2], yv[N / 2];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      u[i] = padd(x[i], x[N - 1 - i]);
+      v[i] = psub(x[i], x[N - 1 - i]);
+    }
+    Jam2<N / 2>::fwd(u, yu);
+    Jam2<N / 2>::fwd(v, yv);
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+      y[2 * k] = yu[k];
+      y[2 * k + 1] = yv[k];
+    }
+  }
+  __device__ __forceinline__ static void inv(const float2* y, float2* x) {
+    float2 ye[N / 2], yo[N / 2], a[N / 2], b[N / 2];
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+      ye[k] = y[2 * k];
+      yo[k] = y[2 * k + 1];
+    }
+    Jam2<N / 2>::inv(ye, a);
+    Jam2<N / 2>::inv(yo, b);
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      x[i] = padd(a[i], b[i]);
+      x[N - 1 - i] = psub(a[i], b[i]);
+    }
+  }
+};
+template <>
+struct Jam2<8> {
+  __device__ __forceinline__ static void fwd(const float2* x, float2* y) { fwd8p(T1Mat(g_jam_unused), x, y); }
+  __device__ __forceinline__ static void inv(const float2* y, float2* x) { inv8p(T1Mat(g_jam_unused), y, x); }
+};
+
+constexpr int kJam2NT = 128;  // threads per CTA: 256 rows = 256 / N blocks per iteration
+#ifndef ADCT_JAM2_MINB16
+#define ADCT_JAM2_MINB16 5
+#endif
+#ifndef ADCT_JAM2_MINB32
+#define ADCT_JAM2_MINB32 4
+#endif
+#ifndef ADCT_JAM2_PF
+#define ADCT_JAM2_PF 1  // L2 prefetch of the next iteration's rows
+#endif
+template <int N>
+constexpr size_t jam2_smem() {  // row-pair tile + weights
+  return (size_t)(kJam2NT * (2 * N + 4) + (N / 2) * (2 * N + 4)) * sizeof(float);
+}
+
+// two horizontally adjacent samples (columns 2cp, 2cp + 1 of one row) as one load
+template <typename SrcT>
+__device__ __forceinline__ float2 ld_pair(const SrcT* p);
+template <>
+__device__ __forceinline__ float2 ld_pair<int16_t>(const int16_t* p) {
+  const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(p));
+  uint32_t lo;
+  asm("prmt.b32 %0, %1, 0, 0x9910;" : "=r"(lo) : "r"(w));  // sign-extended low half
+  return pk((float)(int32_t)lo, (float)((int32_t)w >> 16));
+}
+template <>
+__device__ __forceinline__ float2 ld_pair<uint8_t>(const uint8_t* p) {
+  const uint32_t w = __ldg(reinterpret_cast<const uint16_t*>(p));
+  return psub(pk(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u)),
+                 __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7441u))),
+              pk(8388608.0f, 8388608.0f));
+}
+
+// Thread t of a CTA has two roles over the CTA's 256-row group (256 / N blocks).  COLUMN role
+// (passes 1 and 3): columns 2cp, 2cp + 1 of block t / (N/2) -- one 32-bit (int16) or 16-bit (u8)
+// global access per row holds exactly the pair a packed instruction works on, and the lanes of a
+// warp instruction cover whole 64-byte row segments (two 128-byte wavefronts per 32-point row
+// where the row-per-thread kernel needs sixteen: its LSU data stage, not issue or HBM, was the
+// limiter -- ncu l1tex__data_pipe_lsu_wavefronts 97 %).  ROW role (pass 2): rows 2t, 2t + 1 of the
+// group.  A warp's 32 column pairs and its 64 rows are the same 64 / N blocks, so only __syncwarp
+// separates the passes.  Shared memory holds the group as [row pair][column][2] (pitch 2N + 4
+// floats = an odd number of 16-byte units): every exchange is a conflict-free 128-bit access.
+// The 2-D transform is separable, so columns-then-rows gives the same T X T^T (exact integers
+// forward) and the inverse runs rows-then-columns.
+template <int N, typename SrcT>
+__global__ void __launch_bounds__(kJam2NT, N == 16 ? ADCT_JAM2_MINB16 : ADCT_JAM2_MINB32)
+    jam2_roundtrip_kernel(const SrcT* __restrict__ src, KGeom g, JamW<N> wt, uint32_t nblocks, FastDiv dnbi,
+                          FastDiv dbw, int out_t, int clip, float lo, float hi, void* __restrict__ recon) {
+  constexpr int BPC = 2 * kJam2NT / N;  // blocks per CTA iteration
+  constexpr bool kSat16 = sizeof(SrcT) == 2;
+  constexpr int PP = 2 * N + 4;
+  extern __shared__ __align__(16) float jsm[];
+  float* sm = jsm;
+  float* sw = jsm + kJam2NT * PP;  // sw[rp][l][h] = w[2rp + h][l]
+  for (int t = threadIdx.x; t < N * N; t += kJam2NT) {
+    const int k = t / N, l = t % N;
+    sw[(k >> 1) * PP + 2 * l + (k & 1)] = wt.w[t];
+  }
+  const int t = threadIdx.x;
+  const int bl = t / (N / 2), cp = t % (N / 2);  // column role
+  const uint32_t stride = gridDim.x * BPC;
+  float* rowp = sm + t * PP;                            // row role: rows 2t, 2t + 1 of the group
+  float* colp = sm + (bl * (N / 2)) * PP + 4 * cp;      // column role: + rp * PP
+  const float* wp = sw + (t % (N / 2)) * PP;            // row role: weights of rows 2t % N, + 1
+  uint32_t b = blockIdx.x * BPC + bl;
+  bool valid = b < nblocks;
+  int64_t off = valid ? jam_row_offset<N>(b, 0, g, dnbi, dbw) + 2 * cp : 0;
+  __syncthreads();
+  for (uint32_t b0 = blockIdx.x * BPC; b0 < nblocks; b0 += stride) {
+    {  // pass 1: columns 2cp, 2cp + 1 forward
+      float2 x2[N], y2[N];
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) x2[i] = ld_pair<SrcT>(src + off + (int64_t)i * g.row_stride);
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) x2[i] = pk(0.0f, 0.0f);
+      }
+      Jam2<N>::fwd(x2, y2);
+#pragma unroll
+      for (int rp = 0; rp < N / 2; ++rp)
+        *reinterpret_cast<float4*>(colp + rp * PP) =
+            make_float4(y2[2 * rp].x, y2[2 * rp + 1].x, y2[2 * rp].y, y2[2 * rp + 1].y);
+    }
+    const uint32_t bn = b + stride;  // the next iteration's block: rows 2cp, 2cp + 1 into L2
+    const bool vn = bn < nblocks;
+    const int64_t offn = vn ? jam_row_offset<N>(bn, 0, g, dnbi, dbw) + 2 * cp : 0;
+#if ADCT_JAM2_PF
+    if (vn) {
+      const SrcT* pn = src + offn - 2 * cp + (int64_t)(2 * cp) * g.row_stride;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pn));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + g.row_stride));
+    }
+#endif
+    __syncwarp();
+    {  // pass 2: rows 2t, 2t + 1: forward, weights, inverse
+      float2 z2[N], y2[N];
+#pragma unroll
+      for (int j = 0; j < N; j += 2) {
+        const float4 r4 = *reinterpret_cast<const float4*>(rowp + 2 * j);
+        z2[j] = pk(r4.x, r4.y);
+        z2[j + 1] = pk(r4.z, r4.w);
+      }
+      Jam2<N>::fwd(z2, y2);
+#pragma unroll
+      for (int l = 0; l < N; l += 2) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wp + 2 * l);
+        y2[l] = __fmul2_rn(y2[l], pk(w4.x, w4.y));
+        y2[l + 1] = __fmul2_rn(y2[l + 1], pk(w4.z, w4.w));
+      }
+      Jam2<N>::inv(y2, z2);
+#pragma unroll
+      for (int j = 0; j < N; j += 2)
+        *reinterpret_cast<float4*>(rowp + 2 * j) = make_float4(z2[j].x, z2[j].y, z2[j + 1].x, z2[j + 1].y);
+    }
+    __syncwarp();
+    {  // pass 3: columns 2cp, 2cp + 1 inverse, store
+      float2 c2[N], x2[N];
+#pragma unroll
+      for (int rp = 0; rp < N / 2; ++rp) {
+        const float4 v = *reinterpret_cast<const float4*>(colp + rp * PP);
+        c2[2 * rp] = pk(v.x, v.z);
+        c2[2 * rp + 1] = pk(v.y, v.w);
+      }
+      Jam2<N>::inv(c2, x2);
+      if (valid && kSat16 && out_t == ADCT_I16) {  // int16 -> int16: the saturating pack is the clip
+        uint32_t* o = reinterpret_cast<uint32_t*>(reinterpret_cast<int16_t*>(recon) + off);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const float2 r = padd(x2[i], pk(12582912.0f, 12582912.0f));  // half to even (rint_s32)
+          o[(int64_t)i * (g.row_stride / 2)] = pack_sat_s16((int32_t)(__float_as_uint(r.y) - 0x4B400000u),
+                                                            (int32_t)(__float_as_uint(r.x) - 0x4B400000u));
+        }
+      } else if (valid) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          float va = x2[i].x, vb = x2[i].y;
+          if (clip != ADCT_CLIP_NONE) {
+            va = fminf(fmaxf(va, lo), hi);
+            vb = fminf(fmaxf(vb, lo), hi);
+          }
+          const int64_t o = off + (int64_t)i * g.row_stride;
+          if (out_t == ADCT_F32) {
+            if (clip == ADCT_CLIP_ROUND) {
+              va = rintf(va);
+              vb = rintf(vb);
+            }
+            *reinterpret_cast<float2*>(reinterpret_cast<float*>(recon) + o) = make_float2(va, vb);
+          } else if (out_t == ADCT_I16) {  // already clipped to the source's range (CLIP_ROUND)
+            *reinterpret_cast<uint32_t*>(reinterpret_cast<int16_t*>(recon) + o) =
+                __byte_perm(rbits(va), rbits(vb), 0x5410u);
+          } else {
+            *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(recon) + o) =
+                (uint16_t)__byte_perm(rbits(va), rbits(vb), 0x0040u);
+          }
+        }
+      }
+    }
+    b = bn;
+    valid = vn;
+    off = offn;
+  }
+}
+
 // n x n zig-zag walk (reading A20): anti-diagonals d = k + l in order, even ones bottom-left
 // to top-right
 template <int N>
@@ -410,10 +621,42 @@ adct_status launch_jam(const void* src, const adct_geom& g, int32_t r, void* rec
   kg.n_images = (uint32_t)g.n_images;
   const uint32_t nb = (uint32_t)(g.n_images * kg.nbi);
   if (nb == 0) return ADCT_OK;
-  constexpr int BPC = kJamNT / N;
   int dev = 0, sms = 148, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // the column-pair / row-pair packed kernel (jam2_roundtrip_kernel) is parity-green and issues 39 %
+  // fewer instructions, but runs level with the one-row-per-thread kernel at N = 32 (5.01 vs 4.95 ms)
+  // and slower at N = 16 (4.77 vs 4.52 ms): both sit on the FP32 datapath (23 adds per sample =
+  // 98 % of the HBM time at full FMA-pipe rate) with too few warps to fill it (f2).
+  // ADCT_JAM_V2=1 selects it (tests/test_gpu_parity.py runs the JAM parity suite on it)
+  static const bool v1 = std::getenv("ADCT_JAM_V2") == nullptr || ADCT_JAM_PACKED;
+  if (!v1 && dev >= 0 && dev < kMaxDevices) {
+    constexpr int BPC2 = 2 * kJam2NT / N;
+    constexpr size_t smem = jam2_smem<N>();
+    static std::mutex mu;
+    static int8_t state[kMaxDevices] = {};
+    static int occ2[kMaxDevices] = {};
+    if (!once_per_device(mu, state, [&] {
+          if (cudaFuncSetAttribute(jam2_roundtrip_kernel<N, SrcT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem) != cudaSuccess)
+            return false;
+          int o = 0;
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, jam2_roundtrip_kernel<N, SrcT>, kJam2NT, smem) !=
+                  cudaSuccess || o < 1)
+            o = 1;
+          occ2[dev] = o;
+          return true;
+        }))
+      return ADCT_E_CUDA;
+    const int64_t need2 = ((int64_t)nb + BPC2 - 1) / BPC2, cap2 = (int64_t)sms * occ2[dev];
+    const unsigned grid2 = (unsigned)(need2 < cap2 ? need2 : cap2);
+    jam2_roundtrip_kernel<N, SrcT><<<grid2, kJam2NT, smem, st>>>((const SrcT*)src, kg, wt, nb, make_fastdiv(kg.nbi),
+                                                                 make_fastdiv(kg.bw), (int)recon_t, (int)clip, lo, hi,
+                                                                 recon);
+    count_launch();
+    return launch_status();
+  }
+  constexpr int BPC = kJamNT / N;
   // one wave of resident CTAs: a grid beyond it would leave a second, partly occupied wave
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, jam_roundtrip_kernel<N, SrcT>, kJamNT, 0) != cudaSuccess ||
       occ < 1)

@@ -39,6 +39,7 @@
 #include <mutex>
 
 #include "adct_host.h"
+#include "quant.cuh"
 #include "tc05.cuh"
 #include "tma.cuh"
 
@@ -640,6 +641,198 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (w == 0) tmem_dealloc<kTmemCols>(tbase);
 }
 
+// ---- config 3 on the tensor core: forward + uniform quantiser, u8 planes -> int16 block-major --
+// The same pipeline as fused_u8_tc_kernel (TMA tile = the kind::i8 MMA's A operand, 3 MMA issuers,
+// 12 epilogue warps) with B = all 64 coefficients of both blocks of a pair (N = 64 per half, every
+// Y_kl exact in s32) and an epilogue that quantises (quant.cuh) and writes the block's 128 bytes
+// through a swizzled staging row and one TMA store per (warp, half tile).  Tiles are 1 chunk x 16
+// bands, so TMEM lane p = 8 (band - band0) + pair: the 32 lanes of an epilogue warp are 4 bands x 8
+// pairs, and with the output viewed as {64 codes, 2 halves, W/16 pairs, H/8 bands, images} their
+// blocks 2 pair + h are one box {64, 1, 8, 4, 1} whose rows are the warp's lanes in order.
+constexpr int kTqSlots = 9;
+static_assert(kTqSlots % kTcWays == 0, "slot s only ever holds tiles of issuer s % kTcWays");
+constexpr int kTqNB = 64;
+constexpr int kTqStageBytes = 4096;  // 32 blocks x 128 B per epilogue warp
+constexpr int kTqBBytes = 2 * kTqNB * 128;
+constexpr int kTqBars = 2 * kTqSlots + 4 * kTcDStages;
+constexpr size_t kTqSmem = (size_t)kTqSlots * kTcTileBytes + (size_t)kTcEpiWarps * kTqStageBytes + kTqBBytes +
+                           (size_t)kTqBars * 8 + 16 + 1024;
+static_assert(kTqSmem <= 227 * 1024, "quantiser tensor-core kernel exceeds shared memory");
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    fwd_quant_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tout, TcArgs a,
+                        QTab qt, float stepf, int32_t bh) {
+  constexpr int NB = kTqNB;
+  constexpr uint32_t kIdesc = (2u << 4) | (1u << 10) | ((uint32_t)(NB >> 3) << 17) | (8u << 24);
+  constexpr uint32_t kTmemCols = 512;
+  static_assert(2 * kTcDStages * NB <= (int)kTmemCols, "TMEM columns");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = w & 3;
+  uint8_t* stage = smem + (size_t)kTqSlots * kTcTileBytes;
+  uint8_t* sB = stage + (size_t)kTcEpiWarps * kTqStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kTqBBytes);
+  uint64_t* sfree = full + kTqSlots;
+  uint64_t* dfull = sfree + kTqSlots;
+  uint64_t* dfree = dfull + 2 * kTcDStages;
+  uint32_t* holder = reinterpret_cast<uint32_t*>(dfree + 2 * kTcDStages);
+  // B: row n = 64 blk + 8 k + l holds T_ki T_lj at byte 16 i + 8 blk + j (|b| <= 4)
+  for (int idx = threadIdx.x; idx < 2 * NB * 8; idx += kTcThreads) {
+    const int n = idx >> 3, i = idx & 7;
+    const int blk = n / NB, o = n % NB;
+    const float fki = c_t1f[(o >> 3) * 8 + i];
+    uint32_t lo = 0u, hi = 0u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t b = (uint32_t)(uint8_t)(int8_t)(int)lrintf(fki * c_t1f[(o & 7) * 8 + j]);
+      if (j < 4) lo |= b << (8 * j);
+      else hi |= b << (8 * (j - 4));
+    }
+    *reinterpret_cast<uint4*>(sB + (n >> 3) * 1024 + i * 128 + (n & 7) * 16) =
+        blk ? make_uint4(0u, 0u, lo, hi) : make_uint4(lo, hi, 0u, 0u);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTqSlots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&sfree[i], 1);
+    }
+    for (int i = 0; i < 2 * kTcDStages; ++i) {
+      mbar_init(&dfull[i], 1);
+      mbar_init(&dfree[i], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (w == 0) tmem_alloc<kTmemCols>(smem_u32(holder));
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *holder;
+  const uint32_t full0 = smem_u32(full), ring0 = smem_u32(smem), sB_u = smem_u32(sB);
+
+  if (w == kTcEpiWarps + kTcIssuers) {
+    // ======== TMA producer ========
+    TcPf pf;
+    pf.cg = blockIdx.x;
+    pf_enter(a, pf);
+    uint32_t slot = 0, sph = 0, t = 0;
+#pragma unroll 1
+    for (; pf.cg < a.n_chunks; ++t) {
+      if (t >= (uint32_t)kTqSlots) mbar_wait_sleep(&sfree[slot], sph ^ 1u);
+      if (elect_one()) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + slot * 8),
+                     "r"((uint32_t)kTcTileBytes)
+                     : "memory");
+        tma_load_5d(ring0 + slot * kTcTileBytes, &tmap, 0, 0, pf.trow * 16, pf.tcol, (int32_t)pf.img,
+                    full0 + slot * 8);
+      }
+      __syncwarp();
+      pf_next(a, pf);
+      if (++slot == kTqSlots) {
+        slot = 0;
+        sph ^= 1u;
+      }
+    }
+  } else if (w >= kTcEpiWarps) {
+    // ======== MMA issuers ========
+    const uint32_t iss = (uint32_t)(w - kTcEpiWarps);
+    const uint64_t adesc0 = smem_desc_kmajor(ring0, 128, 1024), bdesc0 = smem_desc_kmajor(sB_u, 128, 1024);
+    uint32_t t = 0;
+#pragma unroll 1
+    for (uint32_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
+      uint32_t img;
+      int32_t tt0;
+      const int32_t n = chunk_tiles(a, cg, img, tt0);
+      const int32_t j0 = (int32_t)((iss + kTcIssuers - t % kTcIssuers) % kTcIssuers);
+#pragma unroll 1
+      for (int32_t j = j0; j < n; j += kTcIssuers) {
+        const uint32_t tt = t + (uint32_t)j;
+        const uint32_t slot = tt % kTqSlots, ds = tt % kTcDStages, dpar = ((tt / kTcDStages) & 1u) ^ 1u;
+        mbar_wait_sleep(&full[slot], (tt / kTqSlots) & 1u);
+        const uint64_t ad = adesc0 + (uint64_t)(slot * (kTcTileBytes >> 4));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t hs = 2 * ds + (uint32_t)h;
+          if (tt >= (uint32_t)kTcDStages) mbar_wait_sleep(&dfree[hs], dpar);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t td = tbase + (uint32_t)NB * hs;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_i8_ss(td, ad + (uint64_t)(kk * 16), bdesc0 + (uint64_t)(h * (NB / 8) * 64 + kk * 16), kIdesc,
+                        kk > 0 ? 1u : 0u);
+            mma_commit(smem_u32(&dfull[hs]));
+            if (h == 1) mma_commit(smem_u32(&sfree[slot]));
+          }
+          __syncwarp();
+        }
+      }
+      t += (uint32_t)n;
+    }
+  } else {
+    // ======== epilogue warps ========
+    const int e = w >> 2;
+    const uint32_t lane_q = (uint32_t)(32 * q) << 16;
+    const uint32_t stg = smem_u32(stage) + (uint32_t)w * kTqStageBytes;
+    const float qru[4] = {qt.ru[0], qt.ru[1], qt.ru[2], qt.ru[3]};
+    const float qri[2] = {qt.ri[0], qt.ri[1]};
+    uint32_t t = 0;
+#pragma unroll 1
+    for (uint32_t cg = blockIdx.x; cg < a.n_chunks; cg += gridDim.x) {
+      uint32_t img;
+      int32_t tt0;
+      const int32_t n = chunk_tiles(a, cg, img, tt0);
+      const int32_t sl = (int32_t)(((uint32_t)e + kTcEpi - t % kTcEpi) % kTcEpi);
+#pragma unroll 1
+      for (int32_t j = sl; j < n; j += kTcEpi) {
+        const uint32_t tt = t + (uint32_t)j;
+        const uint32_t d = tt % kTcDStages, dpar = (tt / kTcDStages) & 1u;
+        const int32_t trow = (int32_t)fdiv((uint32_t)(tt0 + j), a.dtpr);
+        const int32_t tcol = tt0 + j - trow * a.tpr;
+        const int32_t band0 = trow * 16 + 4 * q;  // this warp's 4 bands
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t hs = 2 * d + (uint32_t)h;
+          mbar_wait_sleep(&dfull[hs], dpar);
+          tc_fence_after();
+          const uint32_t tD = tbase + lane_q + (uint32_t)(NB * hs);
+          uint32_t yr[64];
+          tmem_ld32(tD, *reinterpret_cast<uint32_t(*)[32]>(&yr[0]));
+          tmem_ld32(tD + 32, *reinterpret_cast<uint32_t(*)[32]>(&yr[32]));
+          tmem_wait_ld(yr);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dfree[hs]);
+          if (band0 >= bh) continue;  // below the image: zero fill, nothing to write (warp-uniform)
+          float y[64];
+#pragma unroll
+          for (int c = 0; c < 64; ++c) y[c] = __int2float_rn((int32_t)yr[c]);  // exact, |Y| <= 18360
+          uint32_t packed[32];
+          q_block_t1(y, qru, qri, stepf, qt, packed);
+          if (lane == 0) bulk_wait_read<0>();  // the staging rows are free once the previous store read them
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            sts128(stg + (uint32_t)lane * 128u + (((uint32_t)k ^ ((uint32_t)lane & 7u)) << 4),
+                   make_uint4(packed[4 * k], packed[4 * k + 1], packed[4 * k + 2], packed[4 * k + 3]));
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_5d(&tout, 0, h, tcol * 8, band0, (int32_t)img, stg);
+            bulk_commit();
+          }
+        }
+      }
+      t += (uint32_t)n;
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) tmem_dealloc<kTmemCols>(tbase);
+}
+
 template <class MP, int R, int CW>
 bool launch_tc_rc(const CUtensorMap& map, const CUtensorMap& map_d, const TcArgs& a, const DevMat& dm, double* partial,
                   cudaStream_t st) {
@@ -689,7 +882,7 @@ bool launch_tc(int r, int cw, const CUtensorMap& map, const CUtensorMap& map_d, 
 
 // 5-D map {128 B, 8 rows, bands, chunks, images}, strides {row, 8 rows, 128 B, image}; box of
 // bh bands x cw chunks
-bool make_tc_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int bh, int cw) {
+bool make_tc_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int bh, int cw, bool promo128 = false) {
   auto enc = tmap_encoder();
   if (!enc) return false;
   const int64_t istride = g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride;
@@ -699,7 +892,9 @@ bool make_tc_tmap(CUtensorMap* map, const uint8_t* src, const adct_geom& g, int 
   const cuuint32_t box[5] = {128, 8, (cuuint32_t)bh, (cuuint32_t)cw, 1};
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(src), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             // one-chunk boxes: 256-byte promotion would pull the neighbouring chunk too (blockmajor.cu)
+             promo128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -850,6 +1045,66 @@ bool fused_u8_tc_planes(const adct_matrix* m, int n, const uint8_t* const* src, 
     }
     if (*status != ADCT_OK) return true;
   }
+  return true;
+}
+
+// Tensor-core path of approx_dct8x8_fwd_quant (the paper's T1, u8 planes of whole 128-byte chunks,
+// 16-byte aligned strides); false when it does not cover the call (the SIMT TMA kernel then runs).
+bool fwd_quant_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t step, int16_t* q,
+                  cudaStream_t st, adct_status* status) {
+  // Opt-in (ADCT_Q_TC=1): parity-green and 34 % fewer issued instructions than the SIMT TMA kernel
+  // (549 M vs 837 M warp-instructions on config 3), but no faster -- 1.146 vs 1.116 ms: both run at
+  // the same 5.7 TB/s of DRAM traffic, the ceiling of config 3's 1 : 2 read : write mix (read-only
+  // streams at 7.29 TB/s, 1 : 1 copies at 6.2 TB/s), so the SIMT kernel stays the default
+  static const bool off = [] {
+    const char* e = std::getenv("ADCT_Q_TC");
+    return !(e && std::atoi(e) == 1);
+  }();
+  if (off || !m->specialized || g.n_images <= 0 || (g.width % 128) != 0 || (g.height % 8) != 0) return false;
+  if ((g.row_stride % 16) || (g.n_images > 1 && (g.image_stride % 16)) || !aligned(src, 16) || !aligned(q, 128))
+    return false;
+  if (step < 1 || step > 4096) return false;
+  const int64_t nch = g.width / 128, nbd = g.height / 8;
+  const int64_t istride = g.n_images > 1 ? g.image_stride : (int64_t)g.height * g.row_stride;
+  TcArgs a{};
+  a.tpr = (int32_t)nch;
+  a.tpi = (int32_t)(nch * ((nbd + 15) / 16));
+  a.ct = tc_chunk_tiles(a.tpi);
+  a.cpi = (a.tpi + a.ct - 1) / a.ct;
+  const int64_t n_chunks = g.n_images * (int64_t)a.cpi;
+  if (n_chunks >= ((int64_t)1 << 31) || istride >= ((int64_t)1 << 40) || 8 * (int64_t)g.row_stride >= ((int64_t)1 << 40))
+    return false;
+  a.n_chunks = (uint32_t)n_chunks;
+  a.dcpi = make_fastdiv((uint32_t)a.cpi);
+  a.dtpr = make_fastdiv((uint32_t)a.tpr);
+  CUtensorMap map, mout;
+  if (!make_tc_tmap(&map, src, g, 16, 1, true)) return false;
+  {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    const uint64_t bw = (uint64_t)g.width / 8;
+    const cuuint64_t dims[5] = {64, 2, bw / 2, (cuuint64_t)nbd, (cuuint64_t)g.n_images};
+    const cuuint64_t strides[4] = {128, 256, bw * 128, (cuuint64_t)nbd * bw * 128};
+    const cuuint32_t box[5] = {64, 1, 8, 4, 1};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (enc(&mout, CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, q, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  QTab qt;
+  q_fill(qt, step, m->n);
+  static std::mutex mu;
+  static int8_t state[kMaxDevices] = {};
+  if (!once_per_device(mu, state, [] {
+        return cudaFuncSetAttribute(fwd_quant_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kTqSmem) == cudaSuccess;
+      }))
+    return false;
+  const int64_t grid = n_chunks < sms_s() ? n_chunks : sms_s();
+  fwd_quant_tc_kernel<<<(unsigned)grid, kTcThreads, kTqSmem, st>>>(map, mout, a, qt, (float)step, (int32_t)nbd);
+  count_launch();
+  *status = launch_status();
   return true;
 }
 

@@ -84,6 +84,12 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int32_t x, 
                "r"(y), "r"(z), "r"(src)
                : "memory");
 }
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                             int32_t c4, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(src)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until the bulk stores of all but the newest N groups have finished READING shared memory
 template <int N>

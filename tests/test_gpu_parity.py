@@ -694,6 +694,42 @@ def test_jam_full_int16_range(n):
         assert torch.equal(rec.cpu(), x)
 
 
+def test_quantiser_tensor_core_kernel_parity():
+    """The tensor-core quantiser (tc.cu fwd_quant_tc_kernel, selected by ADCT_Q_TC=1 and read once
+    per process) passes the quantiser parity suite -- C3 frames, ties, extremal images -- in a
+    fresh process; widths that are not whole 128-byte chunks still take the SIMT kernel there."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("ADCT_Q_TC"):
+        pytest.skip("already the tensor-core process")
+    env = dict(os.environ, ADCT_Q_TC="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "quant and not tensor_core",
+                        os.path.join(root, "tests", "test_gpu_parity.py")],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
+def test_jam_v2_kernel_parity():
+    """The column-pair / row-pair packed kernel (jam.cu jam2_roundtrip_kernel, selected by
+    ADCT_JAM_V2=1 and read once per process) passes the same oracle parity suite, run in a fresh
+    process (skipped inside that process)."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("ADCT_JAM_V2"):
+        pytest.skip("already the v2 process")
+    env = dict(os.environ, ADCT_JAM_V2="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k",
+                        "jam_roundtrip or jam_full_int16", os.path.join(root, "tests", "test_gpu_parity.py")],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 def test_jam_argument_errors():
     x = torch.zeros((1, 16, 16), dtype=torch.int16, device=DEV)
     with pytest.raises(adct.AdctError):
