@@ -286,6 +286,38 @@ def test_config1_full_size(mats):
             assert abs(psnr[0, r - 1] - oracle.psnr(ref[0, r - 1], 512 * 512)) <= 1e-3
 
 
+def test_config2_full_size_sampled(mats):
+    """C2 in the launch configuration bench.py times: the 45-image 512x512 stack (per-image rho,
+    std of synth.config2_params), r = 1..64, each of the nine matrices through the same call;
+    sampled images (first, last, two inside) against the oracle for every r, and two properties
+    the paper states on the whole stack: at r = 1 all nine matrices give the same error (the DC
+    row of every T is constant, so B_00 and its basis image agree), and the mean PSNR of T1
+    exceeds LO's and T6's for every 1 < r < 64."""
+    rho, std = synth.config2_params(45, 2)
+    imgs = synth.ar1_stack(45, 512, 512, rho, std=std, seed=2, batch=15)
+    d = imgs.to(DEV)
+    rs = list(range(1, 65))
+    pick = [0, 17, 31, 44]
+    mean_psnr = {}
+    sse_r1 = []
+    for name in catalog.CONFIG2_ORDER:
+        sse, psnr = adct.approx_dct8x8_fused_sse(mats[name], d, rs, return_psnr=True)
+        sse, psnr = sse.cpu().numpy(), psnr.cpu().numpy()
+        kw = {"c": M.C} if name == "DCT" else {"t": tmat(name)}
+        ref = oracle.codec_sse(imgs[pick].numpy(), rs, **kw)
+        _check_sse(sse[pick], ref)
+        for j, i in enumerate(pick):
+            for r in (1, 10, 33, 63):
+                assert abs(psnr[i, r - 1] - oracle.psnr(ref[j, r - 1], 512 * 512)) <= 1e-3
+        assert np.all(sse[:, 63] == 0.0) and np.all(np.isposinf(psnr[:, 63]))  # reading A8
+        mean_psnr[name] = psnr[:, :63].mean(axis=0)
+        sse_r1.append(sse[:, 0])
+    for other in sse_r1[1:]:
+        assert np.allclose(other, sse_r1[0], rtol=2e-5, atol=0)
+    assert np.all(mean_psnr["T1"][1:] > mean_psnr["LO"][1:])
+    assert np.all(mean_psnr["T1"][1:] > mean_psnr["T6"][1:])
+
+
 def test_config4_sampled_frames(mats):
     """C4 geometry (3840x2160 luma, 1920x1080 chroma), hot kernel r = 10, on sampled frames;
     per-plane PSNR from the library within 1e-3 dB."""
