@@ -13,6 +13,7 @@
 
 #include "adct_host.h"
 #include "fused_common.cuh"
+#include "packed.cuh"
 
 namespace adct {
 
@@ -109,6 +110,70 @@ __global__ void __launch_bounds__(NT) fused_single_kernel(const SrcT* __restrict
   if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * chunks + blockIdx.x] = tot;
 }
 
+// ---- single r, runtime retention pattern (any matrix, any r) ------------------------------------
+// The retentions that have no compiled kernel used to take the r-list sweep (63 - r rank-one
+// updates per block: 128 4K frames at r = 21 in 3.7 ms).  One pass instead: the packed round trip
+// of packed.cuh with the weight table w = (inverse weight) x (zig-zag keep bit) as a kernel
+// parameter -- kept form for r <= 32 (e = x - x_hat), dropped form for r > 32 (the round trip of the
+// dropped coefficients is x - x_hat itself: exactly 0 at r = 64, reading A17).
+struct WkS {
+  float w[64];
+};
+template <typename SrcT, class MP, int CLIP>
+__device__ __forceinline__ float block_sse_rt(const MP& m, const typename Src<SrcT>::Row (&rows)[8], const float* w,
+                                              bool resid) {
+  float x[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) Src<SrcT>::to_f(rows[i], x[i]);
+  float2 x2[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x2[i][c] = pk(x[i][2 * c], x[i][2 * c + 1]);
+  roundtrip2d_p(m, x2, w);
+  float2 acc[2] = {pk(0.0f, 0.0f), pk(0.0f, 0.0f)};
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float2 xo = pk(x[i][2 * c], x[i][2 * c + 1]), v = x2[i][c];
+      float2 d;
+      if (CLIP == ADCT_CLIP_NONE) {
+        d = resid ? v : psub(xo, v);
+      } else {
+        const float2 xh = resid ? psub(xo, v) : v;
+        d = pk(xo.x - clipv<CLIP>(xh.x, Src<SrcT>::lo, Src<SrcT>::hi),
+               xo.y - clipv<CLIP>(xh.y, Src<SrcT>::lo, Src<SrcT>::hi));
+      }
+      acc[c & 1] = __ffma2_rn(d, d, acc[c & 1]);
+    }
+  return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
+}
+
+template <typename SrcT, class MP, int CLIP>
+__global__ void __launch_bounds__(NT) fused_single_rt_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm, WkS wk,
+                                                             int resid, FastDiv dbw, int32_t chunks,
+                                                             double* __restrict__ partial) {
+  __shared__ double red[NT / 32];
+  const MP m(dm);
+  const SrcT* base = src + (int64_t)blockIdx.y * g.image_stride;
+  const uint32_t q0 = blockIdx.x * (NT * BPT) + threadIdx.x;
+  using Row = typename Src<SrcT>::Row;
+  Row a[8], b[8];
+  double acc = 0.0;
+  if (q0 < g.nbi) load_rows(base, g, dbw, q0, a);
+#pragma unroll 1
+  for (int mb = 0; mb < BPT; mb += 2) {
+    const uint32_t qa = q0 + mb * NT, qb = qa + NT, qc = qb + NT;
+    if (qb < g.nbi) load_rows(base, g, dbw, qb, b);
+    if (qa < g.nbi) acc += (double)block_sse_rt<SrcT, MP, CLIP>(m, a, wk.w, resid != 0);
+    if (mb + 2 < BPT && qc < g.nbi) load_rows(base, g, dbw, qc, a);
+    if (qb < g.nbi) acc += (double)block_sse_rt<SrcT, MP, CLIP>(m, b, wk.w, resid != 0);
+  }
+  const double tot = block_sum<NT>(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)blockIdx.y * chunks + blockIdx.x] = tot;
+}
+
 // ---- config 3: forward with S folded into a uniform quantiser ------------------------------
 // q = sign(Y) floor(|Y| / (step sqrt(n_k n_l)) + 1/2) (reading A10).  fp32 estimate; when the
 // estimate is within 1e-4 of a rounding boundary the exact integer rule
@@ -195,6 +260,24 @@ adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geo
       single = launch_single<SrcT, MP, ADCT_CLIP_NONE>(r_list[0], grid, st, s, kg, m->dev, dbw, chunks, partial);
     else if (!single && clip == ADCT_CLIP)
       single = launch_single<SrcT, MP, ADCT_CLIP>(r_list[0], grid, st, s, kg, m->dev, dbw, chunks, partial);
+    static const bool no_rt = std::getenv("ADCT_NO_SINGLE_RT") != nullptr;  // A/B hook: the r-list sweep instead
+    if (!single && !no_rt) {  // any other r: one pass with a runtime weight table
+      const uint64_t keep = keep_mask(r_list[0]);
+      const bool resid = popc64(keep) > 32;
+      const uint64_t nz = resid ? ~keep : keep;
+      WkS wk;
+      for (int p = 0; p < 64; ++p) wk.w[p] = ((nz >> p) & 1ull) ? m->dev.wy[p] : 0.0f;
+      if (clip == ADCT_CLIP_NONE)
+        fused_single_rt_kernel<SrcT, MP, ADCT_CLIP_NONE><<<grid, NT, 0, st>>>(s, kg, m->dev, wk, (int)resid, dbw,
+                                                                              chunks, partial);
+      else if (clip == ADCT_CLIP)
+        fused_single_rt_kernel<SrcT, MP, ADCT_CLIP><<<grid, NT, 0, st>>>(s, kg, m->dev, wk, (int)resid, dbw, chunks,
+                                                                         partial);
+      else
+        fused_single_rt_kernel<SrcT, MP, ADCT_CLIP_ROUND><<<grid, NT, 0, st>>>(s, kg, m->dev, wk, (int)resid, dbw,
+                                                                               chunks, partial);
+      single = true;
+    }
   }
   dim3 grid((unsigned)chunks, (unsigned)g.n_images);
   int32_t slots = 1;

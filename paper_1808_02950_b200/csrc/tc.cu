@@ -863,8 +863,11 @@ bool launch_tc_r(int cw, const CUtensorMap& map, const CUtensorMap& map_d, const
   }
 }
 
-// compiled (matrix, r) pairs: T1 at config 4's r = 10 and the Lena figures' r = 3, 14
-// (P:L2380-2444); runtime integer matrices at r = 10
+// compiled (matrix, r) pairs: T1 at config 4's r = 10, the Lena figures' r = 3, 14
+// and the other transpose-symmetric zig-zag prefixes that fit the accumulator budget (r <= 16 kept
+// coefficients, or r > 32 with at most 32 dropped: reading A5 lists the symmetric prefixes):
+// 1, 6, 15 and 36; runtime integer matrices at r = 10.  Any other r takes the SIMT kernels.
+constexpr bool tc_r_compiled(int r) { return r == 1 || r == 3 || r == 6 || r == 10 || r == 14 || r == 15 || r == 36; }
 template <class MP>
 bool launch_tc(int r, int cw, const CUtensorMap& map, const CUtensorMap& map_d, const TcArgs& a, const DevMat& dm,
                double* partial, cudaStream_t st) {
@@ -872,9 +875,13 @@ bool launch_tc(int r, int cw, const CUtensorMap& map, const CUtensorMap& map_d, 
     return r == 10 && launch_tc_r<MP, 10>(cw, map, map_d, a, dm, partial, st);
   } else {
     switch (r) {
+      case 1: return launch_tc_r<MP, 1>(cw, map, map_d, a, dm, partial, st);
       case 3: return launch_tc_r<MP, 3>(cw, map, map_d, a, dm, partial, st);
+      case 6: return launch_tc_r<MP, 6>(cw, map, map_d, a, dm, partial, st);
       case 10: return launch_tc_r<MP, 10>(cw, map, map_d, a, dm, partial, st);
       case 14: return launch_tc_r<MP, 14>(cw, map, map_d, a, dm, partial, st);
+      case 15: return launch_tc_r<MP, 15>(cw, map, map_d, a, dm, partial, st);
+      case 36: return launch_tc_r<MP, 36>(cw, map, map_d, a, dm, partial, st);
       default: return false;
     }
   }
@@ -1008,7 +1015,7 @@ bool fused_u8_tc_planes(const adct_matrix* m, int n, const uint8_t* const* src, 
                         double* const* sse, double* const* psnr, double* const* partial, cudaStream_t st,
                         adct_status* status) {
   if (n < 1 || n > kTcMaxPlanes || !m->is_int) return false;
-  const bool r_ok = m->specialized ? (r == 3 || r == 10 || r == 14) : r == 10;
+  const bool r_ok = m->specialized ? tc_r_compiled(r) : r == 10;
   if (!r_ok) return false;
   for (int i = 0; i < n; ++i) {
     const TcPlan p = tc_plan(g[i]);

@@ -66,6 +66,17 @@ def test_stream_every_r_and_matrix(mats, name, r):
     _check(sse, oracle.codec_sse(img.numpy(), [r], t=np.array(catalog.INTEGER[name]).reshape(8, 8)))
 
 
+@pytest.mark.parametrize("r", [1, 3, 6, 14, 15, 36])
+@pytest.mark.parametrize("geom", [(3, 72, 384), (2, 136, 1920), (2, 40, 2048)])
+def test_tensor_core_kernel_other_r(mats, geom, r):
+    """Whole 128-byte chunks: the tensor-core kernel's other compiled retentions for T1 (kept form
+    r <= 15, dropped-coefficient form r = 36) on its three tile shapes (2-chunk, donor, 16-chunk)."""
+    n, h, w = geom
+    img = synth.ar1_field(n, h, w, 0.93, seed=31 * r + w)
+    sse = adct.approx_dct8x8_fused_sse(mats["T1"], img.to(DEV), [r]).cpu().numpy()
+    _check(sse, oracle.codec_sse(img.numpy(), [r], t=M.T1))
+
+
 def test_stream_padded_strides(mats):
     """row_stride > W and image_stride > H*row_stride (16-byte multiples): tensor-map strides."""
     img = synth.uniform_blocks_u8(3, 40, 272, seed=5)
