@@ -116,6 +116,12 @@ __global__ void __launch_bounds__(NT) fused_single_kernel(const SrcT* __restrict
 // of packed.cuh with the weight table w = (inverse weight) x (zig-zag keep bit) as a kernel
 // parameter -- kept form for r <= 32 (e = x - x_hat), dropped form for r > 32 (the round trip of the
 // dropped coefficients is x - x_hat itself: exactly 0 at r = 64, reading A17).
+#ifndef ADCT_RT_RECONVERT
+#define ADCT_RT_RECONVERT 1
+#endif
+#ifndef ADCT_RT_MINB
+#define ADCT_RT_MINB 3  // 168 registers, 12 warps per SM: 0.72-0.89 ms vs 0.84-0.97 (2) and 0.70-0.94 (4, spills) on 128 4K frames
+#endif
 struct WkS {
   float w[64];
 };
@@ -133,7 +139,11 @@ __device__ __forceinline__ float block_sse_rt(const MP& m, const typename Src<Sr
   roundtrip2d_p(m, x2, w);
   float2 acc[2] = {pk(0.0f, 0.0f), pk(0.0f, 0.0f)};
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 8; ++i) {
+#if ADCT_RT_RECONVERT  // the samples again from the raw row instead of 64 registers held across the round trip
+    asm volatile("" : "+r"(*reinterpret_cast<uint32_t*>(const_cast<typename Src<SrcT>::Row*>(&rows[i]))));
+    Src<SrcT>::to_f(rows[i], x[i]);
+#endif
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const float2 xo = pk(x[i][2 * c], x[i][2 * c + 1]), v = x2[i][c];
@@ -147,11 +157,12 @@ __device__ __forceinline__ float block_sse_rt(const MP& m, const typename Src<Sr
       }
       acc[c & 1] = __ffma2_rn(d, d, acc[c & 1]);
     }
+  }
   return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
 }
 
 template <typename SrcT, class MP, int CLIP>
-__global__ void __launch_bounds__(NT) fused_single_rt_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm, WkS wk,
+__global__ void __launch_bounds__(NT, ADCT_RT_MINB) fused_single_rt_kernel(const SrcT* __restrict__ src, KGeom g, DevMat dm, WkS wk,
                                                              int resid, FastDiv dbw, int32_t chunks,
                                                              double* __restrict__ partial) {
   __shared__ double red[NT / 32];
