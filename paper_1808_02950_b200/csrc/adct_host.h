@@ -252,7 +252,7 @@ TcPlan tc_plan(const adct_geom& g);  // tc.cu
 // the tensor-core path for one plane (tc.cu); false when it does not cover the call
 bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
                  double* partial, cudaStream_t st, adct_status* status, int64_t split = 0, double* sse2 = nullptr,
-                 double* psnr2 = nullptr);
+                 double* psnr2 = nullptr, int clip = 0 /* 1: ADCT_CLIP, T1 at r = 10 only */);
 
 // the tensor-core path of approx_dct8x8_fwd_quant (tc.cu); false when it does not cover the call
 bool fwd_quant_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t step, int16_t* q,

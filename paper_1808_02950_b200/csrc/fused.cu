@@ -266,6 +266,14 @@ adct_status fused_dispatch(const adct_matrix* m, const void* src, const adct_geo
         if (fused_u8_stream(m, (const uint8_t*)src, g, r_list[0], sse, psnr, partial, st, &stt)) return stt;
       }
     }
+    if constexpr (std::is_same<SrcT, uint8_t>::value) {
+      // the SPEC's metric policy (clip to [0, 255], no rounding) on the tensor-core kernel: T1, r = 10
+      if (clip == ADCT_CLIP && m->is_int && m->specialized && !g_disable_stream && tc_hot_enabled()) {
+        adct_status stt = ADCT_OK;
+        if (fused_u8_tc(m, (const uint8_t*)src, g, r_list[0], sse, psnr, partial, st, &stt, 0, nullptr, nullptr, 1))
+          return stt;
+      }
+    }
     dim3 grid((unsigned)chunks, (unsigned)g.n_images);
     if (!single && clip == ADCT_CLIP_NONE)
       single = launch_single<SrcT, MP, ADCT_CLIP_NONE>(r_list[0], grid, st, s, kg, m->dev, dbw, chunks, partial);

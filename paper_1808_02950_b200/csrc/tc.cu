@@ -230,9 +230,13 @@ __host__ __device__ constexpr int st_col(int j, int i, int t) {
 
 // ---- one block from its D row (s32 in registers): fp32 inverse and squared error ------------
 // yr: the NY coefficient columns; st: s_i[j] at 8j + i, t_i[j] at 8j + 4 + i (unused for r > 32)
-template <class MP, int R>
+template <class MP, int R, int CLIP = 0>
 __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, const uint32_t* st) {
   using S = TcShape<R>;
+  // CLIP (the reconstruction clipped to [0, 255] before the error, reading A6): the
+  // weights carry an extra 1/510, so q, e, o below are 2 x^ / 510 and one saturating add clips
+  constexpr float kWs = CLIP ? (1.0f / 510.0f) : 1.0f;
+  static_assert(!CLIP || !S::RESID, "the clipped error needs x^ itself: kept form only");
   constexpr uint64_t NZ = S::NZ;
   constexpr uint32_t ROWS = S::ROWS;
   // horizontal inverse of the weighted coefficients, Q = (W o Y') T, rows in ROWS
@@ -243,7 +247,7 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
     float z[8];
 #pragma unroll
     for (int l = 0; l < 8; ++l)
-      z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? i2f(yr[nz_index<NZ>(k * 8 + l)]) * m.wy2(k, l) : 0.0f;
+      z[l] = ((NZ >> (k * 8 + l)) & 1ull) ? i2f(yr[nz_index<NZ>(k * 8 + l)]) * (m.wy2(k, l) * kWs) : 0.0f;
 #define ADCT_TC_ROWINV(K)                                              \
   if (k == K) {                                                        \
     constexpr uint32_t rm = (uint32_t)((NZ >> (8 * K)) & 0xffull);     \
@@ -294,6 +298,23 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
 #endif
       float2 e[4];
       inv8_e2<MP, ROWS>(m, col, e);
+      if constexpr (CLIP != 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 sv = i2f2(st[st_col(j0, i, 0)], st[st_col(j1, i, 0)]);
+          const float2 tv = i2f2(st[st_col(j0, i, 1)], st[st_col(j1, i, 1)]);
+          const float2 o = lsum2<MP, ROWS & 0xaau>([&](int k) { return m.h(i, k); }, col);
+          // clip(2 x^_i, 0, 510) / 510 and the same for x^_(7-i): one FADD.SAT each
+          const float2 ca = f2(__saturatef(e[i].x + o.x), __saturatef(e[i].y + o.y));
+          const float2 cb = f2(__saturatef(e[i].x - o.x), __saturatef(e[i].y - o.y));
+          // 2 (x_i - clip x^_i) = (s_i + t_i) - 510 ca, 2 (x_(7-i) - clip x^_(7-i)) = (s_i - t_i) - 510 cb
+          const float2 da = __ffma2_rn(ca, f2(-510.0f, -510.0f), __fadd2_rn(sv, tv));
+          const float2 db = __ffma2_rn(cb, f2(-510.0f, -510.0f), __fadd2_rn(sv, f2(-tv.x, -tv.y)));
+          a2[i] = __ffma2_rn(da, da, a2[i]);
+          a2[i] = __ffma2_rn(db, db, a2[i]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float2 sv = i2f2(st[st_col(j0, i, 0)], st[st_col(j1, i, 0)]);
@@ -306,9 +327,10 @@ __device__ __forceinline__ float tc_block_sse(const MP& m, const uint32_t* yr, c
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[i] = a2[i].x + a2[i].y;
-    return 0.5f * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+    return (CLIP ? 0.25f : 0.5f) * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
   }
 #endif
+  static_assert(!CLIP || ADCT_TC_PACKED == 1, "the clipped epilogue is written for the packed vertical pass");
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     float col[8];
@@ -409,7 +431,7 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
 // ceil(bands / 16) bands, taken in order, and what is left of them (at most 15 chunk-bands, all
 // in the last band) is one more tile, its 16th KB a fully out-of-bounds box (zero fill).  So a
 // 1920 x 1080 plane is 127 tiles instead of 135 with a 1/16 zero fill each.
-template <class MP, int R, int CW>
+template <class MP, int R, int CW, int CLIP = 0>
 __global__ void __launch_bounds__(kTcThreads, 1)
     fused_u8_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_d, TcArgs a,
                        DevMat dm, double* __restrict__ partial) {
@@ -626,7 +648,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           acc += i2f(yr[0]) + i2f(st[0]);
           continue;
 #endif
-          acc += tc_block_sse<MP, R>(m, yr, st);
+          acc += tc_block_sse<MP, R, CLIP>(m, yr, st);
         }
       }
       float v = acc;  // fixed shuffle order: the partial depends on the geometry only
@@ -833,32 +855,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (w == 0) tmem_dealloc<kTmemCols>(tbase);
 }
 
-template <class MP, int R, int CW>
+template <class MP, int R, int CW, int CLIP = 0>
 bool launch_tc_rc(const CUtensorMap& map, const CUtensorMap& map_d, const TcArgs& a, const DevMat& dm, double* partial,
                   cudaStream_t st) {
   // the shared-memory opt-in is a per-device function attribute: set it once per device
   static std::mutex mu;
   static int8_t state[kMaxDevices] = {};
   if (!once_per_device(mu, state, [] {
-        return cudaFuncSetAttribute(fused_u8_tc_kernel<MP, R, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        return cudaFuncSetAttribute(fused_u8_tc_kernel<MP, R, CW, CLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kTcSmem) == cudaSuccess;
       }))
     return false;
   const int64_t grid = (int64_t)a.n_chunks < sms_s() ? (int64_t)a.n_chunks : sms_s();
-  if (launch_pdl(fused_u8_tc_kernel<MP, R, CW>, dim3((unsigned)grid), dim3(kTcThreads), kTcSmem, st, map, map_d, a,
+  if (launch_pdl(fused_u8_tc_kernel<MP, R, CW, CLIP>, dim3((unsigned)grid), dim3(kTcThreads), kTcSmem, st, map, map_d, a,
                  dm, partial) != cudaSuccess)
     return false;
   return true;
 }
 
-template <class MP, int R>
+template <class MP, int R, int CLIP = 0>
 bool launch_tc_r(int cw, const CUtensorMap& map, const CUtensorMap& map_d, const TcArgs& a, const DevMat& dm,
                  double* partial, cudaStream_t st) {
   switch (cw) {
-    case 2: return launch_tc_rc<MP, R, 2>(map, map_d, a, dm, partial, st);
-    case 1: return launch_tc_rc<MP, R, 1>(map, map_d, a, dm, partial, st);
-    case 16: return launch_tc_rc<MP, R, 16>(map, map_d, a, dm, partial, st);
-    case 15: return launch_tc_rc<MP, R, 15>(map, map_d, a, dm, partial, st);
+    case 2: return launch_tc_rc<MP, R, 2, CLIP>(map, map_d, a, dm, partial, st);
+    case 1: return launch_tc_rc<MP, R, 1, CLIP>(map, map_d, a, dm, partial, st);
+    case 16: return launch_tc_rc<MP, R, 16, CLIP>(map, map_d, a, dm, partial, st);
+    case 15: return launch_tc_rc<MP, R, 15, CLIP>(map, map_d, a, dm, partial, st);
     default: return false;
   }
 }
@@ -870,7 +892,11 @@ bool launch_tc_r(int cw, const CUtensorMap& map, const CUtensorMap& map_d, const
 constexpr bool tc_r_compiled(int r) { return r == 1 || r == 3 || r == 6 || r == 10 || r == 14 || r == 15 || r == 36; }
 template <class MP>
 bool launch_tc(int r, int cw, const CUtensorMap& map, const CUtensorMap& map_d, const TcArgs& a, const DevMat& dm,
-               double* partial, cudaStream_t st) {
+               double* partial, cudaStream_t st, int clip) {
+  if (clip) {  // ADCT_CLIP (the SPEC's metric policy): T1 at config 4's r
+    if constexpr (MP::kConst) return r == 10 && launch_tc_r<MP, 10, 1>(cw, map, map_d, a, dm, partial, st);
+    else return false;
+  }
   if constexpr (!MP::kConst) {
     return r == 10 && launch_tc_r<MP, 10>(cw, map, map_d, a, dm, partial, st);
   } else {
@@ -962,7 +988,8 @@ TcPlan tc_plan(const adct_geom& g) {
 // split > 0: the images are two planes of one geometry stacked in memory (see fused_u8_tc_planes);
 // images [0, split) finalize into sse/psnr, the rest into sse2/psnr2
 bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, int32_t r, double* sse, double* psnr,
-                 double* partial, cudaStream_t st, adct_status* status, int64_t split, double* sse2, double* psnr2) {
+                 double* partial, cudaStream_t st, adct_status* status, int64_t split, double* sse2, double* psnr2,
+                 int clip) {
   const TcPlan p = tc_plan(g);
   if (!p.ok || g.n_images == 0 || !aligned(src, 16) || !m->is_int) return false;
   CUtensorMap map, map_d;
@@ -983,8 +1010,8 @@ bool fused_u8_tc(const adct_matrix* m, const uint8_t* src, const adct_geom& g, i
   a.dmain = p.dmain;
   a.dlast = p.dlast;
   a.dc0 = p.dc0;
-  const bool ok = m->specialized ? launch_tc<T1Mat>(r, p.cw, map, map_d, a, m->dev, partial, st)
-                                 : launch_tc<RtMat>(r, p.cw, map, map_d, a, m->dev, partial, st);
+  const bool ok = m->specialized ? launch_tc<T1Mat>(r, p.cw, map, map_d, a, m->dev, partial, st, clip)
+                                 : launch_tc<RtMat>(r, p.cw, map, map_d, a, m->dev, partial, st, clip);
   if (!ok) return false;
   count_launch();
   if ((*status = launch_status()) != ADCT_OK) return true;

@@ -77,6 +77,27 @@ def test_tensor_core_kernel_other_r(mats, geom, r):
     _check(sse, oracle.codec_sse(img.numpy(), [r], t=M.T1))
 
 
+@pytest.mark.parametrize("kind", ["ar1", "uniform", "extreme"])
+@pytest.mark.parametrize("geom", [(3, 72, 384), (2, 136, 1920), (2, 40, 2048), (1, 2160, 3840)])
+def test_tensor_core_kernel_clip_policy(mats, geom, kind):
+    """ADCT_CLIP (SPEC S:L604: reconstruction clipped to [0, 255], no rounding, before the error;
+    reading A6) on the tensor-core kernel, T1 at r = 10: AR(1) frames, uniform noise, and extremal
+    0 / 255 images whose reconstructions overshoot in most blocks."""
+    n, h, w = geom
+    if kind == "ar1":
+        img = synth.ar1_field(n, h, w, 0.95, seed=h + w)
+    elif kind == "uniform":
+        img = synth.uniform_blocks_u8(n, h, w, seed=h + w)
+    else:
+        img = (torch.randint(0, 2, (n, h, w), generator=torch.Generator().manual_seed(h + w)) * 255).to(torch.uint8)
+    sse = adct.approx_dct8x8_fused_sse(mats["T1"], img.to(DEV), [10], clip=adct.CLIP).cpu().numpy()
+    ref = oracle.codec_sse(img.numpy(), [10], t=M.T1, clip=adct.CLIP)
+    _check(sse, ref)
+    if kind == "extreme":  # the case really exercises the clip: the policies differ by > 10x the 1e-5 tolerance
+        plain = oracle.codec_sse(img.numpy(), [10], t=M.T1)
+        assert np.all(np.abs(plain - ref) > 1e-4 * ref)
+
+
 def test_stream_padded_strides(mats):
     """row_stride > W and image_stride > H*row_stride (16-byte multiples): tensor-map strides."""
     img = synth.uniform_blocks_u8(3, 40, 272, seed=5)
