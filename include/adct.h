@@ -234,7 +234,12 @@ adct_status approx_dct8x8_roundtrip(const adct_matrix* m, const void* src, adct_
  * reading A7).  r_list: HOST array of n_r values in 1..64 (n_r <= 64).
  * sse: device fp64 [n_images][n_r] (required).  psnr: device fp64 [n_images][n_r] or NULL:
  * psnr = 10 log10(255^2 / (sse / (H W))), +inf where sse == 0 (r = 64), computed in fp64 by the
- * library's finalize kernel from the same sum.  workspace >= adct_workspace_bytes(g, n_r). */
+ * library's finalize kernel from the same sum.  workspace >= adct_workspace_bytes(g, n_r).
+ * Kernels (results do not depend on which one runs beyond fp32 rounding order): a single r on u8
+ * planes of whole 128-byte chunks takes the tensor-core kernel for the paper's T1 at
+ * r in {1, 3, 6, 10, 14, 15, 36} without clip and at r = 10 with ADCT_CLIP, and for any other
+ * integer matrix at r = 10 without clip; any other single r takes a one-pass generic kernel;
+ * an r list takes the sweep kernel. */
 adct_status approx_dct8x8_fused_sse(const adct_matrix* m, const void* src, adct_dtype src_t, adct_geom g,
                                     const int32_t* r_list, int32_t n_r, adct_clip clip, double* sse, double* psnr,
                                     void* workspace, size_t workspace_bytes, void* stream);
