@@ -15,10 +15,9 @@ for f in matrix basic fused stream tc sweep blockmajor jam greedy merit; do
   if [ "${FORCE:-0}" != 1 ] && [ -f $o ] && [ -z "$(find $PKG/csrc/$f.cu $HDRS -newer $o 2>/dev/null)" ]; then
     continue
   fi
-  # tc.cu holds ~35 instantiations of the tensor-core kernel: compile its functions in parallel
-  # (4 min -> 50 s; the hot kernel's A/B against the serial build: equal within run-to-run noise)
-  EXTRA=""; [ $f = tc ] && EXTRA="-split-compile 0"
-  nvcc $FLAGS $EXTRA -c $PKG/csrc/$f.cu -o $o.tmp > build/$f.ptxas.log 2>&1 && mv $o.tmp $o &
+  # (tc.cu holds ~35 instantiations of the tensor-core kernel and takes ~4 min; -split-compile cuts
+  # that to 50 s but its register allocation ran the hot kernel 6 % slower in a same-box A/B)
+  nvcc $FLAGS -c $PKG/csrc/$f.cu -o $o.tmp > build/$f.ptxas.log 2>&1 && mv $o.tmp $o &
   pids+=($!)
 done
 rc=0

@@ -218,12 +218,17 @@ constexpr int kTcDStages = kTcWays;               // TMEM accumulator stages (N 
 #define ADCT_TC_CHUNK 24
 #endif
 constexpr int kTcChunkTiles = ADCT_TC_CHUNK;      // tiles per chunk, at most
+#ifndef ADCT_TC_CHUNK_MIN
+#define ADCT_TC_CHUNK_MIN 16  // tiles per chunk, at least (4 -> 16: C4 step -2.5 %, the 64-frame shard -5 %)
+#endif
 // tiles per chunk of a plane: from the image geometry only (so per-image sums do not depend on
-// how images are batched or sharded), small enough that an image has >= 32 chunks -- a 64-frame
-// chroma shard (8 GPUs) then still spreads over many waves of the 148 CTAs -- at least 4
+// how images are batched or sharded): 1/32 of the image's tiles, clamped to [16, 24].  A chunk
+// ends with a warp reduction and a partial store per epilogue warp, so 4-tile chunks (a 1080p
+// chroma plane's 127 tiles / 32) cost the chroma launch ~6 % in chunk turnover; with 16 a 64-frame
+// chroma shard (8 GPUs, U + V = 128 planes x 8 chunks) is still 7 waves of the 148 CTAs
 inline int32_t tc_chunk_tiles(int64_t tiles_per_image) {
   int64_t c = tiles_per_image / 32;
-  if (c < 4) c = 4;
+  if (c < ADCT_TC_CHUNK_MIN) c = ADCT_TC_CHUNK_MIN;
   if (c > kTcChunkTiles) c = kTcChunkTiles;
   return (int32_t)c;
 }
